@@ -1,0 +1,230 @@
+/*
+ * sonarnet_b200 — C ABI of the B200-native eRTIS image-formation path.
+ *
+ * Drop-in boundary for the reference's only caller contract, the pimpl class
+ * `sonarnet::Workspace` (/root/reference/proj/core/include/sonarnet/pipeline.hpp:95-130,
+ * implementation pipeline.cpp:191-591). Plain pointers and sizes only; no
+ * exceptions and no torch types cross this boundary. Every entry point returns
+ * an sn_status that mirrors the reference error taxonomy
+ * (errors.hpp:11-29; CLI exit-code mapping tools/main.cpp:332-350):
+ *
+ *   SN_ERR_CONFIG   <- sonarnet::ConfigError   (Workspace ctor / validate)
+ *   SN_ERR_ARGUMENT <- sonarnet::ArgumentError (beamform shape, geometry)
+ *   SN_ERR_DECODE   <- sonarnet::DecodeError   (process input mismatch)
+ *   SN_ERR_IO       <- sonarnet::IoError
+ *   SN_ERR_CUDA     device / driver failure (no reference analogue)
+ *
+ * The message of the last failure on the calling thread is available from
+ * sn_last_error().
+ *
+ * Threading (pipeline.hpp:95-97): one in-flight call per
+ * workspace; many workspaces may share a device. Each workspace owns one CUDA
+ * stream and all of its device buffers, allocated at creation; process calls
+ * never allocate (allocation_events stays 0, test_pipeline.cpp:143-155).
+ */
+#ifndef SONARNET_B200_H
+#define SONARNET_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SN_CHANNELS 32 /* geometry.hpp:11 kChannelCount */
+#define SN_ABI_VERSION 1
+
+typedef enum sn_status {
+    SN_OK = 0,
+    SN_ERR_CONFIG = 1,
+    SN_ERR_ARGUMENT = 2,
+    SN_ERR_DECODE = 3,
+    SN_ERR_IO = 4,
+    SN_ERR_CUDA = 5,
+    SN_ERR_INTERNAL = 6
+} sn_status;
+
+/* geometry.hpp:65 GridKind */
+typedef enum sn_grid_kind {
+    SN_GRID_HORIZONTAL90 = 0,
+    SN_GRID_BOX1850 = 1,
+    SN_GRID_HEMISPHERE3000 = 2,
+    SN_GRID_CUSTOM = 3
+} sn_grid_kind;
+
+/* Arithmetic of the per-direction stage (beamform, Hilbert envelope,
+ * smoothing). The front end (demodulation, pre-MF decimation) is always the
+ * reference's FP64 arithmetic, bit-exact; the matched filter is FP64. */
+typedef enum sn_precision {
+    SN_PRECISION_F64 = 0, /* FP64 throughout (default) */
+    SN_PRECISION_F32 = 1  /* FP32 per-direction stage, FP64 front end */
+} sn_precision;
+
+/* Flat restatement of sonarnet::PipelineConfig (pipeline.hpp:22-55).
+ * `directions` is borrowed for the duration of sn_workspace_create only. */
+typedef struct sn_pipeline_config {
+    double mic_xyz[SN_CHANNELS * 3]; /* ArrayGeometry positions (x,y,z) m      */
+    const double* directions;        /* n_directions x (azimuth, elevation) rad */
+    uint64_t n_directions;
+    int32_t grid_kind;               /* sn_grid_kind, informational            */
+    int32_t processing_threads;      /* accepted for API parity; unused on GPU */
+    double pdm_rate;                 /* Hz, default 4.5e6                       */
+    double chirp_f_start;            /* Hz, default 90e3                        */
+    double chirp_f_end;              /* Hz, default 25e3                        */
+    double chirp_duration;           /* s,  default 3e-3                        */
+    double demod_cutoff_hz;          /* default 126e3                           */
+    int32_t demod_taps;              /* default 255                             */
+    int32_t demod_decimation;        /* default 10                              */
+    int32_t pre_mf_decimation;       /* default 2                               */
+    int32_t post_envelope_decimation;/* default 10                              */
+    double smoothing_cutoff_hz;      /* default 10e3                            */
+    int32_t smoothing_taps;          /* default 127                             */
+    int32_t precision;               /* sn_precision                            */
+    double speed_of_sound;           /* m/s, default 343                        */
+    double max_range;                /* m, default 5                            */
+} sn_pipeline_config;
+
+/* wire::RawMeasurement (wire.hpp:97-107). `packed` is frame-major, bit index
+ * = frame*channels + channel, MSB first, 1 -> +1 (dsp.hpp:67-69). */
+typedef struct sn_raw_measurement {
+    uint32_t sensor_serial;
+    uint64_t timestamp_us;
+    uint64_t seq;
+    uint16_t channels;
+    uint64_t frames;
+    double pdm_rate;
+    const uint8_t* packed;
+    uint64_t packed_len;
+} sn_raw_measurement;
+
+/* Derived sizes (pipeline.hpp:44-50, pipeline.cpp:40-52, 250-259). */
+typedef struct sn_dims {
+    uint64_t frames;
+    uint64_t demod_samples;
+    uint64_t mf_samples;
+    uint64_t range_bins;
+    uint64_t n_directions;
+    uint64_t ref_len;        /* reference chirp length at the MF rate */
+    uint64_t mf_fft_size;    /* next_pow2(mf_samples + ref_len - 1)   */
+    uint64_t env_fft_size;   /* next_pow2(mf_samples)                  */
+    uint64_t smoothing_len;  /* composite smoothing+anti-alias taps    */
+    double range_bin_size;   /* m */
+    double demod_rate, mf_rate, final_rate;
+    uint64_t max_batch;      /* measurements per device launch          */
+} sn_dims;
+
+/* synth.hpp:13-25 Reflector / Scene. `reflectors` borrowed for the call. */
+typedef struct sn_reflector {
+    double range;
+    double azimuth;
+    double elevation;
+    double reflectivity;
+} sn_reflector;
+
+typedef struct sn_scene {
+    const sn_reflector* reflectors;
+    uint64_t n_reflectors;
+    double noise_rms;
+    uint64_t seed;
+} sn_scene;
+
+typedef struct sn_workspace sn_workspace;
+
+/* Intermediate stage buffers (test / parity access; Workspace::Impl members
+ * pipeline.cpp:211-220). */
+typedef enum sn_stage {
+    SN_STAGE_DEMOD = 0, /* 32 x demod_samples f64 (demod_buf)   */
+    SN_STAGE_PREMF = 1, /* 32 x mf_samples f64    (mf_buf)      */
+    SN_STAGE_FILT = 2   /* 32 x mf_samples f64    (filt_buf)    */
+} sn_stage;
+
+/* ---- library ---------------------------------------------------------- */
+int sn_abi_version(void);
+const char* sn_last_error(void);
+const char* sn_status_name(sn_status s);
+
+/* ---- setup helpers (host only; no GPU needed) ------------------------- */
+/* PipelineConfig defaults + default_array(42) + grid (pipeline.cpp:94-99).
+ * For a built-in grid the direction table is written into `dir_buf`
+ * (capacity in directions) and cfg->directions points at it. */
+sn_status sn_default_config(int32_t grid_kind, sn_pipeline_config* cfg, double* dir_buf,
+                            uint64_t dir_capacity);
+/* geometry.cpp:69-96 default_array(seed) -> 96 doubles */
+sn_status sn_default_array(uint64_t seed, double* mic_xyz_out);
+/* geometry.cpp:181-235 direction_grid(kind) -> n x (az, el) */
+sn_status sn_direction_grid(int32_t grid_kind, double* out, uint64_t capacity,
+                            uint64_t* n_out);
+/* pipeline.cpp:60-92 PipelineConfig::validate + derived sizes. */
+sn_status sn_config_dims(const sn_pipeline_config* cfg, sn_dims* dims);
+/* synth.cpp:116-134 synthesize_measurement: packed bytes of one capture.
+ * `packed_out` must hold 32*frames/8 bytes. */
+sn_status sn_synthesize_packed(const sn_pipeline_config* cfg, const sn_scene* scene,
+                               uint8_t* packed_out, uint64_t capacity);
+
+/* ---- workspace (Workspace, pipeline.hpp:98-130) ------------------------ */
+/* device >= 0: allocate every device buffer on that CUDA device (no
+ * allocation ever happens later). device < 0: host tables only (setup
+ * parity checks on machines without a GPU); process calls then fail with
+ * SN_ERR_CUDA. max_batch: largest batch a single process call may carry. */
+sn_status sn_workspace_create(const sn_pipeline_config* cfg, int device, uint64_t max_batch,
+                              sn_workspace** out);
+void sn_workspace_destroy(sn_workspace* ws);
+sn_status sn_workspace_dims(const sn_workspace* ws, sn_dims* dims);
+
+/* Workspace::process (pipeline.cpp:522-574): host bytes in, host energies
+ * out (n_directions x range_bins f32, row-major). All-or-error. */
+sn_status sn_workspace_process(sn_workspace* ws, const sn_raw_measurement* m,
+                               float* energies_out);
+/* B measurements, identical per-measurement semantics; results do not
+ * depend on B. Validates every measurement before any device work. */
+sn_status sn_workspace_process_batch(sn_workspace* ws, const sn_raw_measurement* ms,
+                                     uint64_t count, float* energies_out);
+/* Device-resident variant: d_packed = count x (32*frames/8) bytes already in
+ * device memory, d_energies = count x n_dirs x bins f32 device buffer.
+ * Enqueued on `stream` (cudaStream_t, NULL = the workspace stream); does not
+ * synchronise. Inputs are trusted (no host-side validation possible). */
+sn_status sn_workspace_process_device(sn_workspace* ws, const uint8_t* d_packed,
+                                      uint64_t count, float* d_energies, void* stream);
+
+/* Workspace::beamform (pipeline.cpp:576-591): filtered = 32 x mf_samples
+ * f64 host, out = n_dirs x mf_samples f64 host. ArgumentError on shape. */
+sn_status sn_workspace_beamform(sn_workspace* ws, const double* filtered, uint64_t channels,
+                                uint64_t samples, double* out);
+
+/* Accessors (pipeline.hpp:108-125). */
+sn_status sn_workspace_delay_table(const sn_workspace* ws, int32_t* out, uint64_t capacity);
+sn_status sn_workspace_reference_advances(const sn_workspace* ws, int32_t* out,
+                                          uint64_t capacity);
+uint64_t sn_workspace_allocation_events(const sn_workspace* ws);
+
+/* Setup tables (host copies), for parity tests of the setup stage. */
+typedef enum sn_table {
+    SN_TABLE_DEMOD_TAPS_REV = 0,   /* demod_rev, demod_taps f64              */
+    SN_TABLE_DEMOD_LUT = 1,        /* 8 x octets x 256 f64                   */
+    SN_TABLE_PREMF_TAPS_REV = 2,   /* premf_rev f64                          */
+    SN_TABLE_CHIRP_REF = 3,        /* reference chirp @ mf rate, ref_len f64 */
+    SN_TABLE_SMOOTH_REV = 4        /* smooth_decimate_rev f64                */
+} sn_table;
+sn_status sn_workspace_table(const sn_workspace* ws, int32_t table, double* out,
+                             uint64_t capacity, uint64_t* n_out);
+
+/* Stage dump of the measurement most recently processed (index `item`
+ * of that batch): sn_stage buffers as f64 host arrays. */
+sn_status sn_workspace_stage(sn_workspace* ws, int32_t stage, uint64_t item, double* out,
+                             uint64_t capacity);
+
+/* Number of kernel launches issued by the last process call (for the bench
+ * `gpu_launches` claim). */
+uint64_t sn_workspace_last_launches(const sn_workspace* ws);
+
+/* CUDA-graph replay of the device path for a fixed (count, d_packed,
+ * d_energies) triple: captured on first use, replayed afterwards. */
+sn_status sn_workspace_process_device_graph(sn_workspace* ws, const uint8_t* d_packed,
+                                            uint64_t count, float* d_energies, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SONARNET_B200_H */

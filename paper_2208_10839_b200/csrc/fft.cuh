@@ -1,0 +1,248 @@
+// CTA-cooperative FFTs over shared memory (sm_100a).
+//
+// Replaces the reference's FFTW calls on the hot path (fft.cpp:81-92 RealFft
+// forward/inverse, reached from pipeline.cpp:558-560 for the matched filter
+// and :454-461 for the Hilbert envelope). FFTW conventions are kept:
+// forward e^{-i}, unnormalised; the inverse is scaled by 1/n (fft.cpp:87-92).
+//
+// Layout: a real signal of N = 2M samples is viewed as M complex points
+// z[n] = x[2n] + i x[2n+1] and transformed by an M-point complex Stockham FFT
+// (radix-16 passes, one radix-2/4/8 pass to finish); a split/merge step maps
+// Z <-> the half spectrum X[0..M]. Complex scratch lives in shared memory with
+// one pad element per 16 (index i -> i + i/16) so that the strided Stockham
+// stores are bank-conflict free for 16-byte elements.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace snb {
+
+template <typename R> struct Cx;
+template <> struct Cx<double> { using T = double2; };
+template <> struct Cx<float> { using T = float2; };
+
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+
+template <typename V> __device__ __forceinline__ V cadd(V a, V b) { return {a.x + b.x, a.y + b.y}; }
+template <typename V> __device__ __forceinline__ V csub(V a, V b) { return {a.x - b.x, a.y - b.y}; }
+template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
+    return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+}
+template <typename V> __device__ __forceinline__ V cconj(V a) { return {a.x, -a.y}; }
+// multiply by -i (forward) or +i (inverse)
+template <bool INV, typename V> __device__ __forceinline__ V rot90(V a) {
+    return INV ? V{-a.y, a.x} : V{a.y, -a.x};
+}
+
+template <bool INV, typename V>
+__device__ __forceinline__ void dft2(V& a, V& b) {
+    const V t = a;
+    a = cadd(t, b);
+    b = csub(t, b);
+}
+
+template <bool INV, typename V>
+__device__ __forceinline__ void dft4(V& x0, V& x1, V& x2, V& x3) {
+    const V a = cadd(x0, x2), b = csub(x0, x2);
+    const V c = cadd(x1, x3), d = rot90<INV>(csub(x1, x3));
+    x0 = cadd(a, c);
+    x2 = csub(a, c);
+    x1 = cadd(b, d);
+    x3 = csub(b, d);
+}
+
+// Constant twiddles e^{-+2 pi i k/16}
+template <bool INV, typename V, typename R>
+__device__ __forceinline__ V tw16(V v, int k) {
+    constexpr R c1 = (R)0.92387953251128675613, s1 = (R)0.38268343236508977173;
+    constexpr R h = (R)0.70710678118654752440;
+    const R sg = INV ? (R)1 : (R)-1; // sign of the sine term
+    switch (k & 15) {
+        case 0: return v;
+        case 1: return cmul(v, V{c1, sg * s1});
+        case 2: return cmul(v, V{h, sg * h});
+        case 3: return cmul(v, V{s1, sg * c1});
+        case 4: return rot90<INV>(v);
+        case 6: return cmul(v, V{-h, sg * h});
+        case 9: return cmul(v, V{-c1, -sg * s1});
+        default: {
+            // not used by the 4x4 decomposition (n2*k1 in {0,1,2,3,4,6,9})
+            return v;
+        }
+    }
+}
+
+template <bool INV, typename V>
+__device__ __forceinline__ void dft8(V* x) {
+    using R = decltype(x[0].x);
+    // radix-2 x 4: even/odd split
+    dft4<INV>(x[0], x[2], x[4], x[6]);
+    dft4<INV>(x[1], x[3], x[5], x[7]);
+    constexpr R h = (R)0.70710678118654752440;
+    const R sg = INV ? (R)1 : (R)-1;
+    // twiddle odd outputs by W8^k
+    const V o1 = cmul(x[3], V{h, sg * h});
+    const V o2 = rot90<INV>(x[5]);
+    const V o3 = cmul(x[7], V{-h, sg * h});
+    const V e0 = x[0], e1 = x[2], e2 = x[4], e3 = x[6], o0 = x[1];
+    x[0] = cadd(e0, o0);
+    x[4] = csub(e0, o0);
+    x[1] = cadd(e1, o1);
+    x[5] = csub(e1, o1);
+    x[2] = cadd(e2, o2);
+    x[6] = csub(e2, o2);
+    x[3] = cadd(e3, o3);
+    x[7] = csub(e3, o3);
+}
+
+// In-register 16-point DFT (4x4 Cooley-Tukey). Input natural order; the
+// output is left TRANSPOSED: register 4*k1 + k2 holds X[k1 + 4*k2]
+// (see out_slot), which saves a 16-element register shuffle.
+template <bool INV, typename V>
+__device__ __forceinline__ void dft16(V* x) {
+    using R = decltype(x[0].x);
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4<INV>(x[n2], x[4 + n2], x[8 + n2], x[12 + n2]);
+    // x[4*k1 + n2] = T[k1][n2]; twiddle by W16^{n2*k1}
+#pragma unroll
+    for (int k1 = 1; k1 < 4; ++k1) {
+#pragma unroll
+        for (int n2 = 1; n2 < 4; ++n2) x[4 * k1 + n2] = tw16<INV, V, R>(x[4 * k1 + n2], n2 * k1);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4<INV>(x[4 * k1], x[4 * k1 + 1], x[4 * k1 + 2], x[4 * k1 + 3]);
+}
+
+// Output index held by register slot i after dft_r<RADIX>.
+template <int RADIX>
+__device__ __forceinline__ constexpr int out_slot(int i) {
+    return RADIX == 16 ? (i >> 2) + 4 * (i & 3) : i;
+}
+
+template <int RADIX, bool INV, typename V>
+__device__ __forceinline__ void dft_r(V* x) {
+    if constexpr (RADIX == 16) dft16<INV>(x);
+    else if constexpr (RADIX == 8) dft8<INV>(x);
+    else if constexpr (RADIX == 4) dft4<INV>(x[0], x[1], x[2], x[3]);
+    else dft2<INV>(x[0], x[1]);
+}
+
+// One Stockham pass: radix RADIX, current sub-transform length ns.
+// src element i at src[SRC_PADDED ? pad16(i) : i]; dst always padded.
+// twM = e^{-2 pi i k / M} table, stride `tws` (table may be for a larger size).
+// In place (src == dst) is allowed: every thread loads all of its inputs
+// before a CTA barrier, then stores.
+template <int RADIX, bool INV, bool SRC_PADDED, typename V>
+__device__ __forceinline__ void stockham_pass(const V* src, V* dst, int M, int ns,
+                                              const V* __restrict__ tw, int tws) {
+    const int nj = M / RADIX;
+    const int j = threadIdx.x;
+    V v[RADIX];
+    const bool active = j < nj;
+    if (active) {
+#pragma unroll
+        for (int r = 0; r < RADIX; ++r) {
+            const int i = j + r * nj;
+            v[r] = src[SRC_PADDED ? pad16(i) : i];
+        }
+        const int k = j % ns;
+        if (ns > 1) {
+            const int step = (M / (ns * RADIX)) * k; // twiddle index per r
+#pragma unroll
+            for (int r = 1; r < RADIX; ++r) {
+                V w = tw[(size_t)(step * r) * tws];
+                if (INV) w.y = -w.y;
+                v[r] = cmul(v[r], w);
+            }
+        }
+        dft_r<RADIX, INV>(v);
+    }
+    __syncthreads();
+    if (active) {
+        const int k = j % ns;
+        const int base = (j / ns) * ns * RADIX + k;
+#pragma unroll
+        for (int r = 0; r < RADIX; ++r) dst[pad16(base + out_slot<RADIX>(r) * ns)] = v[r];
+    }
+    __syncthreads();
+}
+
+// Full M-point complex FFT (M = 2^m, 16 <= M <= 16*blockDim). The first pass
+// reads `src` (padded or not), all later passes work in place on `buf`.
+template <bool INV, bool SRC_PADDED, typename V>
+__device__ void cfft(const V* src, V* buf, int M, const V* __restrict__ tw, int tws) {
+    int ns = 1;
+    bool first = true;
+    int rem = M;
+    while (rem >= 16) {
+        if (first) stockham_pass<16, INV, SRC_PADDED>(src, buf, M, ns, tw, tws);
+        else stockham_pass<16, INV, true>(buf, buf, M, ns, tw, tws);
+        first = false;
+        ns *= 16;
+        rem /= 16;
+    }
+    if (rem > 1) {
+        if (rem == 8) {
+            if (first) stockham_pass<8, INV, SRC_PADDED>(src, buf, M, ns, tw, tws);
+            else stockham_pass<8, INV, true>(buf, buf, M, ns, tw, tws);
+        } else if (rem == 4) {
+            if (first) stockham_pass<4, INV, SRC_PADDED>(src, buf, M, ns, tw, tws);
+            else stockham_pass<4, INV, true>(buf, buf, M, ns, tw, tws);
+        } else {
+            if (first) stockham_pass<2, INV, SRC_PADDED>(src, buf, M, ns, tw, tws);
+            else stockham_pass<2, INV, true>(buf, buf, M, ns, tw, tws);
+        }
+    }
+}
+
+// Split/merge between the M-point complex transform of a packed real signal
+// and its half spectrum, fused with a per-bin spectral operator, then merged
+// back for the inverse real transform (all in place in padded `buf`).
+//   forward:  X[k] = E[k] + W_N^k O[k],  E = (Z_k + Z*_{M-k})/2, O = (Z_k - Z*_{M-k})/(2i)
+//   op:       Y[k] = op(X[k], k)         (must keep Y Hermitian-consistent)
+//   inverse:  Z'[k] = E' + i O',  E' = (Y_k + Y*_{M-k})/2, O' = (Y_k - Y*_{M-k}) conj(W_N^k)/2
+// twN = e^{-2 pi i k / N} for k in [0, M].
+template <typename V, typename Op>
+__device__ __forceinline__ void real_spectral_op(V* buf, int M, const V* __restrict__ twN, Op op) {
+    using R = decltype(V{}.x);
+    for (int k = threadIdx.x; k <= M / 2; k += blockDim.x) {
+        if (k == 0) {
+            const V z0 = buf[0];
+            const V x0 = {z0.x + z0.y, (R)0};
+            const V xm = {z0.x - z0.y, (R)0};
+            const V y0 = op(x0, 0);
+            const V ym = op(xm, M);
+            // imag(Y[0]), imag(Y[M]) ignored (FFTW c2r convention)
+            const R e = (R)0.5 * (y0.x + ym.x);
+            const R o = (R)0.5 * (y0.x - ym.x);
+            buf[0] = V{e, o};
+            continue;
+        }
+        const int kk = M - k;
+        const V zk = buf[pad16(k)], zkk = buf[pad16(kk)];
+        const V wk = twN[k], wkk = twN[kk];
+        // forward split
+        const V ek = {(R)0.5 * (zk.x + zkk.x), (R)0.5 * (zk.y - zkk.y)};
+        const V dk = {(R)0.5 * (zk.x - zkk.x), (R)0.5 * (zk.y + zkk.y)}; // (Z_k - Z*_kk)/2
+        const V ok = {dk.y, -dk.x};                                    // / i
+        const V xk = cadd(ek, cmul(wk, ok));
+        const V ekk = {ek.x, -ek.y};       // E_{M-k} = conj(E_k)
+        const V okk = {ok.x, -ok.y};       // O_{M-k} = conj(O_k)
+        const V xkk = cadd(ekk, cmul(wkk, okk));
+        const V yk = op(xk, k), ykk = op(xkk, kk);
+        // inverse merge
+        const V e2 = {(R)0.5 * (yk.x + ykk.x), (R)0.5 * (yk.y - ykk.y)};
+        const V d2 = {(R)0.5 * (yk.x - ykk.x), (R)0.5 * (yk.y + ykk.y)};
+        const V o2 = cmul(d2, cconj(wk));
+        buf[pad16(k)] = V{e2.x - o2.y, e2.y + o2.x};
+        if (kk != k) {
+            const V e3 = {(R)0.5 * (ykk.x + yk.x), (R)0.5 * (ykk.y - yk.y)};
+            const V d3 = {(R)0.5 * (ykk.x - yk.x), (R)0.5 * (ykk.y + yk.y)};
+            const V o3 = cmul(d3, cconj(wkk));
+            buf[pad16(kk)] = V{e3.x - o3.y, e3.y + o3.x};
+        }
+    }
+    __syncthreads();
+}
+
+} // namespace snb

@@ -1,0 +1,348 @@
+// Hot-path kernels; see kernels.cuh for the stage map and layouts.
+#include "fft.cuh"
+#include "kernels.cuh"
+
+#include <cstdio>
+
+namespace snb {
+
+// ---------------------------------------------------------------------------
+// k_demod: bit transpose + FP64 LUT demodulation, bit-exact with
+// pipeline.cpp:352-430.
+//
+// The output index m of channel c reads the 255-frame window starting at
+// s = D*m - center; with P = 8/gcd(D,8), every m of one residue class
+// r = m mod P shares the bit alignment a = s & 7, so a CTA serves one class
+// and keeps that alignment's 33 x 256 FP64 table (67.6 KB) in shared memory
+// for its whole life (persistent grid over (measurement, block of m)).
+// Frames are transposed into per-channel MSB-first rows with warp ballots:
+// lane l holds frame word l, ballot over channel c's bit yields 32 frames of
+// channel c. The sum per output follows the reference exactly: four lanes
+// over octets t = 0 .. 4*floor(T/4)-1 (lane t mod 4), (a0+a1)+(a2+a3), then
+// the remaining octets in order; adds only, every add rounded (DADD).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_demod(DemodArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* lut = reinterpret_cast<double*>(smem);
+    uint32_t* rows = reinterpret_cast<uint32_t*>(lut + (size_t)a.octets * 256);
+    const int r = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    if (r >= a.demod_len) return;
+    const int64_t s_r = (int64_t)a.decim * r - a.center;
+    const int align = (int)(((s_r % 8) + 8) % 8);
+    {
+        const double* src = a.lut + (size_t)align * a.octets * 256;
+        for (int i = threadIdx.x; i < a.octets * 256; i += blockDim.x) lut[i] = src[i];
+    }
+    const int64_t P = a.period;
+    const int64_t Jr = (a.demod_len - r + P - 1) / P; // outputs of class r
+    const int64_t nblk = (Jr + a.jblock - 1) / a.jblock;
+    const int64_t items = nblk * a.batch;
+    const int T = a.octets;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int64_t b = it / nblk, jb = it % nblk;
+        const int64_t j0 = jb * a.jblock, j1 = min(Jr, j0 + a.jblock);
+        // j range whose m lies in [m_lo, m_hi)
+        int64_t jv0 = a.m_lo > r ? (a.m_lo - r + P - 1) / P : 0;
+        int64_t jv1 = a.m_hi > r ? (a.m_hi - r + P - 1) / P : 0;
+        jv0 = max(jv0, j0);
+        jv1 = min(jv1, j1);
+        int64_t F0 = 0;
+        __syncthreads(); // rows of the previous item fully consumed
+        if (jv0 < jv1) {
+            const int64_t s_first = (int64_t)a.decim * (r + P * jv0) - a.center;
+            const int64_t s_last = (int64_t)a.decim * (r + P * (jv1 - 1)) - a.center;
+            F0 = s_first & ~int64_t(31);
+            const int64_t F1 = s_last + a.taps;
+            const int nwords = (int)((F1 - F0 + 31) / 32) + 2; // +2: octet over-read
+            const uint8_t* pk = a.packed + b * a.packed_bytes;
+            for (int g = warp; g < nwords && g < a.words; g += nwarps) {
+                const int64_t f = F0 + 32 * (int64_t)g + lane;
+                const uint32_t w = f < a.frames ? *reinterpret_cast<const uint32_t*>(pk + 4 * f) : 0u;
+                uint32_t mine = 0;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    // channel c: byte c/8 of the frame word, bit 7 - c%8 (MSB first)
+                    const uint32_t m = __ballot_sync(0xffffffffu, (w >> ((c & ~7) + 7 - (c & 7))) & 1u);
+                    if (lane == c) mine = m;
+                }
+                // bit f of `mine` = frame F0+32g+f; row bytes are MSB-first per 8 frames
+                rows[lane * a.words + g] = __byte_perm(__brev(mine), 0, 0x0123);
+            }
+        }
+        __syncthreads();
+        const int64_t nj = j1 - j0;
+        double* out_b = a.demod + (size_t)b * 32 * a.demod_len;
+        for (int64_t q = threadIdx.x; q < 32 * nj; q += blockDim.x) {
+            const int c = (int)(q / nj);
+            const int64_t m = r + P * (j0 + q % nj);
+            double v = 0.0;
+            if (m >= a.m_lo && m < a.m_hi) {
+                const int64_t s = (int64_t)a.decim * m - a.center;
+                const uint8_t* rb =
+                    reinterpret_cast<const uint8_t*>(rows + c * a.words) + ((s - F0) >> 3);
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                int t = 0;
+                for (; t + 4 <= T; t += 4) {
+                    a0 = __dadd_rn(a0, lut[(t + 0) * 256 + rb[t + 0]]);
+                    a1 = __dadd_rn(a1, lut[(t + 1) * 256 + rb[t + 1]]);
+                    a2 = __dadd_rn(a2, lut[(t + 2) * 256 + rb[t + 2]]);
+                    a3 = __dadd_rn(a3, lut[(t + 3) * 256 + rb[t + 3]]);
+                }
+                double acc = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+                for (; t < T; ++t) acc = __dadd_rn(acc, lut[t * 256 + rb[t]]);
+                v = acc;
+            }
+            out_b[(size_t)c * a.demod_len + m] = v;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_premf: pre-MF anti-alias FIR + decimation (strided_filter, filters.hpp:
+// 14-39, called at pipeline.cpp:551-553), bit-exact: the same clipped window,
+// the same four-lane order, products rounded before the add (no FMA).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_premf(PremfArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* taps = reinterpret_cast<double*>(smem);
+    double* xs = taps + a.taps;
+    const int ch = blockIdx.y, b = blockIdx.z;
+    const int64_t n0 = (int64_t)blockIdx.x * blockDim.x;
+    const int64_t start = -(int64_t)((a.taps - 1) / 2);
+    const double* x = a.demod + ((size_t)b * 32 + ch) * a.demod_len;
+    for (int i = threadIdx.x; i < a.taps; i += blockDim.x) taps[i] = a.rev[i];
+    const int64_t s0 = start + n0 * a.decim;
+    const int span = (int)(blockDim.x - 1) * a.decim + a.taps;
+    for (int i = threadIdx.x; i < span; i += blockDim.x) {
+        const int64_t g = s0 + i;
+        xs[i] = (g >= 0 && g < a.demod_len) ? x[g] : 0.0;
+    }
+    __syncthreads();
+    const int64_t n = n0 + threadIdx.x;
+    if (n >= a.mf_len) return;
+    const int64_t s = start + n * a.decim;
+    const int64_t lo = (s > 0 ? s : (int64_t)0), hi = ((s + a.taps) < a.demod_len ? (s + a.taps) : a.demod_len);
+    const double* h = taps + (lo - s);
+    const double* xv = xs + (lo - s0);
+    const int cnt = (int)(hi - lo);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int j = 0;
+    for (; j + 4 <= cnt; j += 4) {
+        a0 = __dadd_rn(a0, __dmul_rn(h[j], xv[j]));
+        a1 = __dadd_rn(a1, __dmul_rn(h[j + 1], xv[j + 1]));
+        a2 = __dadd_rn(a2, __dmul_rn(h[j + 2], xv[j + 2]));
+        a3 = __dadd_rn(a3, __dmul_rn(h[j + 3], xv[j + 3]));
+    }
+    double acc = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+    for (; j < cnt; ++j) acc = __dadd_rn(acc, __dmul_rn(h[j], xv[j]));
+    a.mf[((size_t)b * 32 + ch) * a.mf_len + n] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// k_matched_filter: per (channel, measurement) row, FP64 real FFT of the
+// zero-padded row, product with the spectrum of the reversed chirp, inverse,
+// 1/N, and the window [ref_len-1, ref_len-1+mf_len) (pipeline.cpp:555-562).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_matched_filter(MfArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int N = a.n, M = N / 2;
+    double* bufA = reinterpret_cast<double*>(smem);
+    double2* bufB = reinterpret_cast<double2*>(bufA + N);
+    const size_t row = (size_t)blockIdx.y * 32 + blockIdx.x;
+    const double* x = a.mf + row * a.mf_len;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) bufA[i] = i < a.mf_len ? x[i] : 0.0;
+    __syncthreads();
+    cfft<false, false>(reinterpret_cast<const double2*>(bufA), bufB, M, a.tw, 2);
+    const double scale = 2.0 / (double)N;
+    const double2* R = a.ref_spec;
+    real_spectral_op(bufB, M, a.tw, [&](double2 X, int k) {
+        return cmul(X, double2{R[k].x * scale, R[k].y * scale});
+    });
+    cfft<true, true>(bufB, bufB, M, a.tw, 2);
+    double* out = a.filt + row * a.mf_len;
+    float* out32 = a.filt32 ? a.filt32 + row * a.mf_len : nullptr;
+    for (int64_t n = threadIdx.x; n < a.mf_len; n += blockDim.x) {
+        const int64_t q = n + a.ref_len - 1;
+        const double2 z = bufB[pad16((int)(q >> 1))];
+        const double v = (q & 1) ? z.y : z.x;
+        out[n] = v;
+        if (out32) out32[n] = (float)v;
+    }
+}
+
+// Forward real FFT of one length-n row (setup: spectrum of the reversed chirp).
+__global__ void __launch_bounds__(kThreads) k_rfft_forward(const double* x, double2* X,
+                                                           const double2* tw, int N) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int M = N / 2;
+    double* bufA = reinterpret_cast<double*>(smem);
+    double2* bufB = reinterpret_cast<double2*>(bufA + N);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) bufA[i] = x[i];
+    __syncthreads();
+    cfft<false, false>(reinterpret_cast<const double2*>(bufA), bufB, M, tw, 2);
+    for (int k = threadIdx.x; k <= M; k += blockDim.x) {
+        const int k1 = k % M, k2 = (M - k) % M;
+        const double2 zk = bufB[pad16(k1)], zkk = bufB[pad16(k2)];
+        const double2 e = {0.5 * (zk.x + zkk.x), 0.5 * (zk.y - zkk.y)};
+        const double2 d = {0.5 * (zk.x - zkk.x), 0.5 * (zk.y + zkk.y)};
+        const double2 o = {d.y, -d.x};
+        X[k] = cadd(e, cmul(tw[k], o));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_directions<R>: one (measurement, direction) per iteration of a persistent
+// CTA: delay-and-sum (pipeline.cpp:432-446) into shared memory, Hilbert
+// transform via a real FFT pair with DC and Nyquist zeroed and X -> -iX
+// (pipeline.cpp:448-461), |x + iH(x)| (:462-464), the 447-tap composite
+// smoothing/anti-alias FIR at stride 10 (:466-468, filters.hpp:14-39) and the
+// clamp/float write-out (:469-471).
+// R = double reproduces the reference arithmetic (beam bit-exact, spectral
+// stages within FP64 rounding); R = float is the F32 mode.
+// ---------------------------------------------------------------------------
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_directions(DirArgs a) {
+    using V = typename Cx<R>::T;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int N = a.n, M = N / 2;
+    R* bufA = reinterpret_cast<R*>(smem);                    // N real
+    V* bufB = reinterpret_cast<V*>(bufA + N);                // M + M/16 complex
+    R* comp = reinterpret_cast<R*>(bufB + M + M / 16);       // comp_len
+    int* sh = reinterpret_cast<int*>(comp + a.comp_len);     // 32 shifts
+    const R* filt = reinterpret_cast<const R*>(a.filt);
+    const R* cr = reinterpret_cast<const R*>(a.comp);
+    const V* tw = reinterpret_cast<const V*>(a.tw);
+    for (int i = threadIdx.x; i < a.comp_len; i += blockDim.x) comp[i] = cr[i];
+    const int64_t L = a.mf_len;
+    const int64_t items = a.n_dirs * a.batch;
+    const R scale = (R)2 / (R)N;
+    const int c0 = (a.comp_len - 1) / 2;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int64_t b = it / a.n_dirs, d = it % a.n_dirs;
+        if (threadIdx.x < 32) sh[threadIdx.x] = a.shifts[d * 32 + threadIdx.x];
+        __syncthreads();
+        // delay-and-sum, channels accumulated in order 0..31 then * (1/32)
+        const R* fb = filt + (size_t)b * 32 * L;
+        for (int64_t n = threadIdx.x; n < N; n += blockDim.x) {
+            R acc = 0;
+            if (n < L) {
+#pragma unroll 8
+                for (int i = 0; i < 32; ++i) {
+                    const int64_t src = n - sh[i];
+                    if (src >= 0 && src < L) acc += fb[(size_t)i * L + src];
+                }
+                acc *= (R)(1.0 / 32.0);
+            }
+            bufA[n] = acc;
+        }
+        __syncthreads();
+        cfft<false, false>(reinterpret_cast<const V*>(bufA), bufB, M, tw, 2);
+        real_spectral_op(bufB, M, tw, [&](V X, int k) {
+            if (k == 0 || k == M) return V{(R)0, (R)0};
+            return V{X.y * scale, -X.x * scale}; // -i X, with the 2/N of the inverse
+        });
+        cfft<true, true>(bufB, bufB, M, tw, 2);
+        for (int64_t n = threadIdx.x; n < L; n += blockDim.x) {
+            const V z = bufB[pad16((int)(n >> 1))];
+            const R h = (n & 1) ? z.y : z.x;
+            const R bv = bufA[n];
+            bufA[n] = sqrt(bv * bv + h * h);
+        }
+        __syncthreads();
+        float* eo = a.energy + (size_t)it * a.bins;
+        for (int64_t k = threadIdx.x; k < a.bins; k += blockDim.x) {
+            const int64_t s = k * a.decim - c0;
+            const int64_t lo = s > 0 ? s : 0, hi = ((s + a.comp_len) < L ? (s + a.comp_len) : L);
+            const R* hh = comp + (lo - s);
+            const R* xx = bufA + lo;
+            const int cnt = (int)(hi - lo);
+            R a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            int j = 0;
+            for (; j + 4 <= cnt; j += 4) {
+                a0 += hh[j] * xx[j];
+                a1 += hh[j + 1] * xx[j + 1];
+                a2 += hh[j + 2] * xx[j + 2];
+                a3 += hh[j + 3] * xx[j + 3];
+            }
+            R acc = (a0 + a1) + (a2 + a3);
+            for (; j < cnt; ++j) acc += hh[j] * xx[j];
+            const float v = (float)acc;
+            eo[k] = v > 0.0f ? v : 0.0f;
+        }
+        __syncthreads();
+    }
+}
+
+// Workspace::beamform accessor (pipeline.cpp:576-591): materialised beams
+// [n_dirs][L] f64, channels accumulated in order then * (1/32).
+__global__ void __launch_bounds__(kThreads) k_beamform(const double* filt, double* beams,
+                                                      const int32_t* shifts, int64_t L) {
+    const int64_t d = blockIdx.y;
+    __shared__ int sh[32];
+    if (threadIdx.x < 32) sh[threadIdx.x] = shifts[d * 32 + threadIdx.x];
+    __syncthreads();
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= L) return;
+    double acc = 0.0;
+    for (int i = 0; i < 32; ++i) {
+        const int64_t src = n - sh[i];
+        if (src >= 0 && src < L) acc += filt[(size_t)i * L + src];
+    }
+    beams[d * L + n] = acc * (1.0 / 32.0);
+}
+
+void launch_beamform(const double* filt, double* beams, const int32_t* shifts, int64_t L,
+                     int64_t n_dirs, cudaStream_t s) {
+    k_beamform<<<dim3((unsigned)((L + kThreads - 1) / kThreads), (unsigned)n_dirs), kThreads, 0, s>>>(
+        filt, beams, shifts, L);
+}
+
+// ---------------------------------------------------------------------------
+size_t demod_smem_bytes(int octets, int words) {
+    return (size_t)octets * 256 * sizeof(double) + (size_t)32 * words * sizeof(uint32_t);
+}
+
+size_t fft_smem_bytes(int n, int real_bytes) {
+    const int M = n / 2;
+    return (size_t)n * real_bytes + (size_t)(M + M / 16) * 2 * real_bytes;
+}
+
+static void set_smem(const void* fn, size_t smem) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+void launch_demod(const DemodArgs& a, int grid_x, size_t smem, cudaStream_t s) {
+    set_smem((const void*)k_demod, smem);
+    k_demod<<<dim3(grid_x, a.period), kThreads, smem, s>>>(a);
+}
+
+void launch_premf(const PremfArgs& a, int batch, cudaStream_t s) {
+    const size_t smem = (size_t)(a.taps + (kThreads - 1) * a.decim + a.taps) * sizeof(double);
+    set_smem((const void*)k_premf, smem);
+    const int gx = (int)((a.mf_len + kThreads - 1) / kThreads);
+    k_premf<<<dim3(gx, 32, batch), kThreads, smem, s>>>(a);
+}
+
+void launch_matched_filter(const MfArgs& a, int batch, size_t smem, cudaStream_t s) {
+    set_smem((const void*)k_matched_filter, smem);
+    k_matched_filter<<<dim3(32, batch), kThreads, smem, s>>>(a);
+}
+
+void launch_directions_f64(const DirArgs& a, int grid, size_t smem, cudaStream_t s) {
+    set_smem((const void*)k_directions<double>, smem);
+    k_directions<double><<<grid, kThreads, smem, s>>>(a);
+}
+
+void launch_directions_f32(const DirArgs& a, int grid, size_t smem, cudaStream_t s) {
+    set_smem((const void*)k_directions<float>, smem);
+    k_directions<float><<<grid, kThreads, smem, s>>>(a);
+}
+
+void launch_rfft_forward(const double* x, double2* X, const double2* tw, int n, size_t smem,
+                         cudaStream_t s) {
+    set_smem((const void*)k_rfft_forward, smem);
+    k_rfft_forward<<<1, kThreads, smem, s>>>(x, X, tw, n);
+}
+
+} // namespace snb

@@ -1,0 +1,79 @@
+// Hot-path kernels of the eRTIS image-formation pipeline (sm_100a).
+//
+// One measurement = 32 channels of packed 1-bit PDM (frame-major); output =
+// n_dirs x bins f32 energyscape. Reference: sonarnet::Workspace::process
+// (pipeline.cpp:522-574). Stage -> kernel:
+//   transpose_bits + demodulate_channel (pipeline.cpp:352-430) -> k_demod
+//   strided_filter pre-MF /2         (filters.hpp:14-39)      -> k_premf
+//   matched filter via RealFft       (pipeline.cpp:555-562)    -> k_matched_filter
+//   run_directions: beamform_into + envelope_direction
+//                                    (pipeline.cpp:432-505)    -> k_directions
+// Device layouts (batch index b outermost):
+//   packed  [b][frames*4 bytes]           u8   (as received)
+//   demod   [b][32][demod_len]            f64
+//   mf      [b][32][mf_len]               f64
+//   filt    [b][32][mf_len]               f64  (+ f32 copy in F32 mode)
+//   energy  [b][n_dirs][bins]             f32
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace snb {
+
+constexpr int kThreads = 256;
+
+struct DemodArgs {
+    const uint8_t* packed;    // [B][packed_bytes]
+    double* demod;            // [B][32][demod_len]
+    const double* lut;        // [8][octets][256]
+    int64_t frames, packed_bytes, demod_len, m_lo, m_hi;
+    int taps, decim, center, octets, period; // period P = 8/gcd(D,8)
+    int jblock;               // outputs (of one class) per work item
+    int words;                // row words per channel staged in smem
+    int batch;
+};
+
+struct PremfArgs {
+    const double* demod; // [B][32][demod_len]
+    double* mf;          // [B][32][mf_len]
+    const double* rev;   // premf reversed taps
+    int64_t demod_len, mf_len;
+    int taps, decim;
+};
+
+struct MfArgs {
+    const double* mf;       // [B][32][mf_len]
+    double* filt;           // [B][32][mf_len]
+    float* filt32;          // optional f32 copy (F32 mode) or null
+    const double2* ref_spec;// M+1 bins of rfft(reversed chirp, N)
+    const double2* tw;      // e^{-2 pi i k/N}, k < N
+    int64_t mf_len;
+    int n, ref_len;
+};
+
+struct DirArgs {
+    const void* filt;        // [B][32][mf_len] f64 or f32
+    float* energy;           // [B][n_dirs][bins]
+    const int32_t* shifts;   // [n_dirs][32] = delay - advance
+    const void* comp;        // composite reversed kernel (f64 or f32)
+    const void* tw;          // twiddles for N (double2 or float2)
+    int64_t mf_len, bins, n_dirs;
+    int n, comp_len, decim, batch;
+};
+
+void launch_demod(const DemodArgs& a, int grid_x, size_t smem, cudaStream_t s);
+void launch_premf(const PremfArgs& a, int batch, cudaStream_t s);
+void launch_matched_filter(const MfArgs& a, int batch, size_t smem, cudaStream_t s);
+void launch_directions_f64(const DirArgs& a, int grid, size_t smem, cudaStream_t s);
+void launch_directions_f32(const DirArgs& a, int grid, size_t smem, cudaStream_t s);
+void launch_rfft_forward(const double* x, double2* X, const double2* tw, int n, size_t smem,
+                         cudaStream_t s);
+
+void launch_beamform(const double* filt, double* beams, const int32_t* shifts, int64_t L,
+                     int64_t n_dirs, cudaStream_t s);
+
+size_t demod_smem_bytes(int octets, int words);
+size_t fft_smem_bytes(int n, int real_bytes);
+
+} // namespace snb

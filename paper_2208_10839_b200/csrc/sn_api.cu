@@ -1,0 +1,576 @@
+// C ABI (include/sonarnet_b200.h) over the device pipeline.
+//
+// sn_workspace is the B200 counterpart of sonarnet::Workspace::Impl
+// (pipeline.cpp:191-319): everything is derived and allocated at creation
+// (device tables, per-stage buffers for max_batch measurements, pinned
+// staging, one CUDA stream); process calls only enqueue kernels and copies.
+#include "kernels.cuh"
+#include "plan.hpp"
+#include "sonarnet_b200.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+using namespace snb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaError : Error {
+    explicit CudaError(const std::string& w) : Error(SN_ERR_CUDA, w) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+template <typename F>
+sn_status guarded(F&& f) {
+    try {
+        f();
+        return SN_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SN_ERR_INTERNAL;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (dev >= 0) {
+            cudaGetDevice(&prev);
+            if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+        }
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+T* dmalloc(size_t n, uint64_t& count) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, std::max<size_t>(1, n) * sizeof(T)), "cudaMalloc");
+    ++count;
+    return static_cast<T*>(p);
+}
+
+template <typename T>
+void upload(T* d, const std::vector<T>& h, cudaStream_t s) {
+    ck(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s), "upload");
+}
+
+std::vector<double2> twiddles(uint64_t n) {
+    std::vector<double2> tw(n);
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    for (uint64_t k = 0; k < n; ++k) {
+        const long double a = two_pi * (long double)k / (long double)n;
+        tw[k] = double2{(double)cosl(a), (double)-sinl(a)};
+    }
+    return tw;
+}
+
+} // namespace
+
+struct sn_workspace {
+    Plan plan;
+    int device = -1;
+    uint64_t max_batch = 1;
+    cudaStream_t stream = nullptr;
+    bool f32 = false;
+    // device buffers
+    uint8_t* d_packed = nullptr;
+    double* d_demod = nullptr;
+    double* d_mf = nullptr;
+    double* d_filt = nullptr;
+    float* d_filt32 = nullptr;
+    float* d_energy = nullptr;
+    double* d_lut = nullptr;
+    double* d_premf = nullptr;
+    double* d_comp = nullptr;
+    float* d_comp32 = nullptr;
+    int32_t* d_shifts = nullptr;
+    double2* d_ref_spec = nullptr;
+    double2* d_tw_mf = nullptr;
+    double2* d_tw_env = nullptr;
+    float2* d_tw_env32 = nullptr;
+    uint8_t* h_in = nullptr;
+    float* h_out = nullptr;
+    // launch shapes
+    DemodArgs demod{};
+    int demod_grid = 0;
+    size_t demod_smem = 0, mf_smem = 0, dir_smem = 0;
+    int dir_grid = 0;
+    uint64_t packed_bytes = 0, energy_per = 0;
+    uint64_t alloc_events = 0, device_allocs = 0, last_launches = 0;
+    // graph cache
+    cudaGraphExec_t graph = nullptr;
+    const uint8_t* g_in = nullptr;
+    float* g_out = nullptr;
+    uint64_t g_count = 0;
+
+    ~sn_workspace() {
+        if (device < 0) return;
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        if (graph) cudaGraphExecDestroy(graph);
+        for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
+                        (void*)d_filt32, (void*)d_energy, (void*)d_lut, (void*)d_premf,
+                        (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
+                        (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32}) {
+            if (p) cudaFree(p);
+        }
+        if (h_in) cudaFreeHost(h_in);
+        if (h_out) cudaFreeHost(h_out);
+        if (stream) cudaStreamDestroy(stream);
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+
+    void require_device() const {
+        if (device < 0) throw CudaError("workspace was created without a device (device < 0)");
+    }
+
+    void init_device() {
+        const Sizes& s = plan.sz;
+        if (s.mf_fft > 8192 || s.env_fft > 8192) {
+            config_error("pipeline: FFT size " + std::to_string(std::max(s.mf_fft, s.env_fft)) +
+                         " exceeds the shared-memory FFT limit (8192; max_range <= ~5.8 m at 4.5 MHz)");
+        }
+        if (s.mf_fft < 32 || s.env_fft < 32) config_error("pipeline: processed window too short for the device FFT");
+        DeviceGuard g(device);
+        ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        packed_bytes = static_cast<uint64_t>(kCh) * s.frames / 8;
+        energy_per = s.n_dirs * s.bins;
+        const uint64_t B = max_batch;
+        uint64_t& n = device_allocs;
+        d_packed = dmalloc<uint8_t>(B * packed_bytes, n);
+        d_demod = dmalloc<double>(B * kCh * s.demod_len, n);
+        d_mf = dmalloc<double>(B * kCh * s.mf_len, n);
+        d_filt = dmalloc<double>(B * kCh * s.mf_len, n);
+        if (f32) d_filt32 = dmalloc<float>(B * kCh * s.mf_len, n);
+        d_energy = dmalloc<float>(B * energy_per, n);
+        d_lut = dmalloc<double>(plan.demod_lut.size(), n);
+        d_premf = dmalloc<double>(plan.premf_rev.size(), n);
+        d_comp = dmalloc<double>(plan.comp_rev.size(), n);
+        d_comp32 = dmalloc<float>(plan.comp_rev.size(), n);
+        d_shifts = dmalloc<int32_t>(s.n_dirs * kCh, n);
+        d_ref_spec = dmalloc<double2>(s.mf_fft / 2 + 1, n);
+        d_tw_mf = dmalloc<double2>(s.mf_fft, n);
+        d_tw_env = dmalloc<double2>(s.env_fft, n);
+        d_tw_env32 = dmalloc<float2>(s.env_fft, n);
+        ck(cudaMallocHost(&h_in, B * packed_bytes), "cudaMallocHost");
+        ck(cudaMallocHost(&h_out, B * energy_per * sizeof(float)), "cudaMallocHost");
+
+        upload(d_lut, plan.demod_lut, stream);
+        upload(d_premf, plan.premf_rev, stream);
+        upload(d_comp, plan.comp_rev, stream);
+        std::vector<float> comp32(plan.comp_rev.begin(), plan.comp_rev.end());
+        upload(d_comp32, comp32, stream);
+        std::vector<int32_t> shifts(s.n_dirs * kCh);
+        for (uint64_t d = 0; d < s.n_dirs; ++d) {
+            for (int i = 0; i < kCh; ++i) shifts[d * kCh + i] = plan.delays[d * kCh + i] - plan.advances[d];
+        }
+        upload(d_shifts, shifts, stream);
+        const auto tw_mf = twiddles(s.mf_fft), tw_env = twiddles(s.env_fft);
+        upload(d_tw_mf, tw_mf, stream);
+        upload(d_tw_env, tw_env, stream);
+        std::vector<float2> tw32(s.env_fft);
+        for (uint64_t k = 0; k < s.env_fft; ++k) tw32[k] = float2{(float)tw_env[k].x, (float)tw_env[k].y};
+        upload(d_tw_env32, tw32, stream);
+        // reference spectrum: rfft of the reversed chirp zero-padded to mf_fft
+        // (pipeline.cpp:274-278)
+        {
+            std::vector<double> padded(s.mf_fft, 0.0);
+            std::reverse_copy(plan.chirp_ref.begin(), plan.chirp_ref.end(), padded.begin());
+            double* d_tmp = nullptr;
+            ck(cudaMalloc(&d_tmp, padded.size() * sizeof(double)), "cudaMalloc");
+            upload(d_tmp, padded, stream);
+            mf_smem = fft_smem_bytes((int)s.mf_fft, sizeof(double));
+            launch_rfft_forward(d_tmp, d_ref_spec, d_tw_mf, (int)s.mf_fft, mf_smem, stream);
+            ck(cudaGetLastError(), "rfft launch");
+            ck(cudaStreamSynchronize(stream), "setup sync");
+            cudaFree(d_tmp);
+        }
+        // demod launch shape
+        const int D = plan.cfg.demod_decimation;
+        const int P = 8 / std::gcd(D, 8);
+        demod = DemodArgs{};
+        demod.lut = d_lut;
+        demod.frames = (int64_t)s.frames;
+        demod.packed_bytes = (int64_t)packed_bytes;
+        demod.demod_len = (int64_t)s.demod_len;
+        demod.m_lo = s.m_lo;
+        demod.m_hi = s.m_hi;
+        demod.taps = plan.cfg.demod_taps;
+        demod.decim = D;
+        demod.center = (plan.cfg.demod_taps - 1) / 2;
+        demod.octets = (int)s.lut_octets;
+        demod.period = P;
+        demod.jblock = 64;
+        int words = (int)((int64_t)D * P * (demod.jblock - 1) + demod.taps + 62) / 32 + 3;
+        if (words % 2 == 0) ++words;
+        demod.words = words;
+        demod_smem = demod_smem_bytes(demod.octets, words);
+        if (demod_smem > 227 * 1024) {
+            config_error("pipeline: demod taps " + std::to_string(demod.taps) + " exceed the shared-memory LUT limit");
+        }
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        const int per_sm = std::max(1, (int)((228 * 1024) / (demod_smem + 1024)));
+        demod_grid = std::max(1, sms * per_sm / P);
+        dir_smem = fft_smem_bytes((int)s.env_fft, f32 ? sizeof(float) : sizeof(double)) +
+                   plan.comp_rev.size() * (f32 ? sizeof(float) : sizeof(double)) + 32 * sizeof(int);
+        const int dir_per_sm = std::max(1, (int)((228 * 1024) / (dir_smem + 1024)));
+        dir_grid = sms * dir_per_sm;
+        mf_smem = fft_smem_bytes((int)s.mf_fft, sizeof(double));
+        ck(cudaStreamSynchronize(stream), "setup sync");
+    }
+
+    // Enqueue the whole pipeline for `count` measurements (count <= max_batch).
+    void enqueue(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s) {
+        const Sizes& z = plan.sz;
+        DemodArgs da = demod;
+        da.packed = d_in;
+        da.demod = d_demod;
+        da.batch = (int)count;
+        launch_demod(da, demod_grid, demod_smem, s);
+        PremfArgs pa{d_demod, d_mf, d_premf, (int64_t)z.demod_len, (int64_t)z.mf_len,
+                     (int)plan.premf_rev.size(), plan.cfg.pre_mf_decimation};
+        launch_premf(pa, (int)count, s);
+        MfArgs ma{d_mf, d_filt, f32 ? d_filt32 : nullptr, d_ref_spec, d_tw_mf,
+                  (int64_t)z.mf_len, (int)z.mf_fft, (int)z.ref_len};
+        launch_matched_filter(ma, (int)count, mf_smem, s);
+        DirArgs ra{};
+        ra.filt = f32 ? (const void*)d_filt32 : (const void*)d_filt;
+        ra.energy = d_out;
+        ra.shifts = d_shifts;
+        ra.comp = f32 ? (const void*)d_comp32 : (const void*)d_comp;
+        ra.tw = f32 ? (const void*)d_tw_env32 : (const void*)d_tw_env;
+        ra.mf_len = (int64_t)z.mf_len;
+        ra.bins = (int64_t)z.bins;
+        ra.n_dirs = (int64_t)z.n_dirs;
+        ra.n = (int)z.env_fft;
+        ra.comp_len = (int)plan.comp_rev.size();
+        ra.decim = plan.cfg.post_envelope_decimation;
+        ra.batch = (int)count;
+        const int grid = (int)std::min<int64_t>(dir_grid, (int64_t)(z.n_dirs * count));
+        if (f32) launch_directions_f32(ra, grid, dir_smem, s);
+        else launch_directions_f64(ra, grid, dir_smem, s);
+        ck(cudaGetLastError(), "kernel launch");
+        last_launches = 4;
+    }
+
+    void validate(const sn_raw_measurement& m) const { // pipeline.cpp:524-540
+        const Sizes& z = plan.sz;
+        if (m.channels != kCh) {
+            decode_error("process: measurement has " + std::to_string(m.channels) +
+                         " channels, expected " + std::to_string(kCh));
+        }
+        if (m.frames != z.frames) {
+            decode_error("process: measurement has " + std::to_string(m.frames) +
+                         " frames, config expects " + std::to_string(z.frames));
+        }
+        if (std::abs(m.pdm_rate - plan.cfg.pdm_rate) > 1e-6 * plan.cfg.pdm_rate) {
+            decode_error("process: measurement pdm_rate " + std::to_string(m.pdm_rate) +
+                         " does not match config " + std::to_string(plan.cfg.pdm_rate));
+        }
+        const uint64_t expected = static_cast<uint64_t>(kCh) * z.frames / 8;
+        if (m.packed_len != expected || m.packed == nullptr) {
+            decode_error("process: payload is " + std::to_string(m.packed_len) +
+                         " bytes, expected " + std::to_string(expected));
+        }
+    }
+
+    void process_host(const sn_raw_measurement* ms, uint64_t count, float* out) {
+        require_device();
+        for (uint64_t i = 0; i < count; ++i) validate(ms[i]); // all-or-error
+        DeviceGuard g(device);
+        uint64_t done = 0;
+        while (done < count) {
+            const uint64_t c = std::min(max_batch, count - done);
+            for (uint64_t i = 0; i < c; ++i) {
+                std::memcpy(h_in + i * packed_bytes, ms[done + i].packed, packed_bytes);
+            }
+            ck(cudaMemcpyAsync(d_packed, h_in, c * packed_bytes, cudaMemcpyHostToDevice, stream), "H2D");
+            enqueue(d_packed, c, d_energy, stream);
+            ck(cudaMemcpyAsync(h_out, d_energy, c * energy_per * sizeof(float), cudaMemcpyDeviceToHost,
+                               stream), "D2H");
+            ck(cudaStreamSynchronize(stream), "process sync");
+            std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
+            done += c;
+        }
+    }
+
+    void process_device(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s) {
+        require_device();
+        DeviceGuard g(device);
+        if (!s) s = stream;
+        uint64_t done = 0;
+        while (done < count) {
+            const uint64_t c = std::min(max_batch, count - done);
+            enqueue(d_in + done * packed_bytes, c, d_out + done * energy_per, s);
+            done += c;
+        }
+    }
+};
+
+extern "C" {
+
+int sn_abi_version(void) { return SN_ABI_VERSION; }
+const char* sn_last_error(void) { return g_last_error.c_str(); }
+
+const char* sn_status_name(sn_status s) {
+    switch (s) {
+        case SN_OK: return "ok";
+        case SN_ERR_CONFIG: return "config";
+        case SN_ERR_ARGUMENT: return "argument";
+        case SN_ERR_DECODE: return "decode";
+        case SN_ERR_IO: return "io";
+        case SN_ERR_CUDA: return "cuda";
+        default: return "internal";
+    }
+}
+
+sn_status sn_default_array(uint64_t seed, double* out) {
+    return guarded([&] {
+        if (!out) argument_error("null output");
+        default_array(seed, out);
+    });
+}
+
+sn_status sn_direction_grid(int32_t kind, double* out, uint64_t capacity, uint64_t* n_out) {
+    return guarded([&] {
+        const auto g = direction_grid(kind);
+        const uint64_t n = g.size() / 2;
+        if (n_out) *n_out = n;
+        if (!out) return;
+        if (capacity < n) argument_error("direction buffer too small");
+        std::copy(g.begin(), g.end(), out);
+    });
+}
+
+sn_status sn_default_config(int32_t kind, sn_pipeline_config* cfg, double* dir_buf,
+                            uint64_t dir_capacity) {
+    return guarded([&] {
+        if (!cfg) argument_error("null config");
+        default_config(kind, cfg);
+        if (kind != SN_GRID_CUSTOM) {
+            const auto g = direction_grid(kind);
+            const uint64_t n = g.size() / 2;
+            if (!dir_buf || dir_capacity < n) argument_error("direction buffer too small");
+            std::copy(g.begin(), g.end(), dir_buf);
+            cfg->directions = dir_buf;
+            cfg->n_directions = n;
+        }
+    });
+}
+
+sn_status sn_config_dims(const sn_pipeline_config* cfg, sn_dims* dims) {
+    return guarded([&] {
+        if (!cfg || !dims) argument_error("null argument");
+        const Sizes s = derive_sizes(*cfg);
+        *dims = sn_dims{s.frames, s.demod_len, s.mf_len, s.bins, s.n_dirs, s.ref_len, s.mf_fft,
+                        s.env_fft, s.comp_len, s.range_bin_size, s.demod_rate, s.mf_rate,
+                        s.final_rate, 0};
+    });
+}
+
+sn_status sn_synthesize_packed(const sn_pipeline_config* cfg, const sn_scene* scene,
+                               uint8_t* packed_out, uint64_t capacity) {
+    return guarded([&] {
+        if (!cfg || !scene || !packed_out) argument_error("null argument");
+        const Sizes s = derive_sizes(*cfg);
+        if (capacity < static_cast<uint64_t>(kCh) * s.frames / 8) argument_error("packed buffer too small");
+        synthesize_packed(*cfg, *scene, packed_out);
+    });
+}
+
+sn_status sn_workspace_create(const sn_pipeline_config* cfg, int device, uint64_t max_batch,
+                              sn_workspace** out) {
+    return guarded([&] {
+        if (!cfg || !out) argument_error("null argument");
+        *out = nullptr;
+        auto ws = std::make_unique<sn_workspace>();
+        ws->plan = make_plan(*cfg);
+        ws->device = device;
+        ws->max_batch = std::max<uint64_t>(1, max_batch);
+        ws->f32 = cfg->precision == SN_PRECISION_F32;
+        if (cfg->precision != SN_PRECISION_F64 && cfg->precision != SN_PRECISION_F32) {
+            config_error("pipeline: unknown precision mode");
+        }
+        if (device >= 0) ws->init_device();
+        *out = ws.release();
+    });
+}
+
+void sn_workspace_destroy(sn_workspace* ws) { delete ws; }
+
+sn_status sn_workspace_dims(const sn_workspace* ws, sn_dims* dims) {
+    return guarded([&] {
+        if (!ws || !dims) argument_error("null argument");
+        const Sizes& s = ws->plan.sz;
+        *dims = sn_dims{s.frames, s.demod_len, s.mf_len, s.bins, s.n_dirs, s.ref_len, s.mf_fft,
+                        s.env_fft, s.comp_len, s.range_bin_size, s.demod_rate, s.mf_rate,
+                        s.final_rate, ws->max_batch};
+    });
+}
+
+sn_status sn_workspace_process(sn_workspace* ws, const sn_raw_measurement* m, float* out) {
+    return guarded([&] {
+        if (!ws || !m || !out) argument_error("null argument");
+        ws->process_host(m, 1, out);
+    });
+}
+
+sn_status sn_workspace_process_batch(sn_workspace* ws, const sn_raw_measurement* ms,
+                                     uint64_t count, float* out) {
+    return guarded([&] {
+        if (!ws || (!ms && count) || (!out && count)) argument_error("null argument");
+        if (count) ws->process_host(ms, count, out);
+    });
+}
+
+sn_status sn_workspace_process_device(sn_workspace* ws, const uint8_t* d_packed, uint64_t count,
+                                      float* d_energies, void* stream) {
+    return guarded([&] {
+        if (!ws || (!d_packed && count) || (!d_energies && count)) argument_error("null argument");
+        ws->process_device(d_packed, count, d_energies, static_cast<cudaStream_t>(stream));
+    });
+}
+
+sn_status sn_workspace_process_device_graph(sn_workspace* ws, const uint8_t* d_packed,
+                                            uint64_t count, float* d_energies, void* stream) {
+    return guarded([&] {
+        if (!ws || !d_packed || !d_energies || count == 0) argument_error("null argument");
+        ws->require_device();
+        if (count > ws->max_batch) argument_error("graph replay: count exceeds max_batch");
+        DeviceGuard g(ws->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ws->stream;
+        if (!ws->graph || ws->g_in != d_packed || ws->g_out != d_energies || ws->g_count != count) {
+            if (ws->graph) {
+                cudaGraphExecDestroy(ws->graph);
+                ws->graph = nullptr;
+            }
+            cudaGraph_t graph;
+            ck(cudaStreamBeginCapture(ws->stream, cudaStreamCaptureModeThreadLocal), "capture");
+            ws->enqueue(d_packed, count, d_energies, ws->stream);
+            ck(cudaStreamEndCapture(ws->stream, &graph), "capture end");
+            ck(cudaGraphInstantiate(&ws->graph, graph, 0), "graph instantiate");
+            cudaGraphDestroy(graph);
+            ws->g_in = d_packed;
+            ws->g_out = d_energies;
+            ws->g_count = count;
+        }
+        ck(cudaGraphLaunch(ws->graph, s), "graph launch");
+        ws->last_launches = 4;
+    });
+}
+
+sn_status sn_workspace_delay_table(const sn_workspace* ws, int32_t* out, uint64_t capacity) {
+    return guarded([&] {
+        if (!ws || !out) argument_error("null argument");
+        if (capacity < ws->plan.delays.size()) argument_error("buffer too small");
+        std::copy(ws->plan.delays.begin(), ws->plan.delays.end(), out);
+    });
+}
+
+sn_status sn_workspace_reference_advances(const sn_workspace* ws, int32_t* out, uint64_t capacity) {
+    return guarded([&] {
+        if (!ws || !out) argument_error("null argument");
+        if (capacity < ws->plan.advances.size()) argument_error("buffer too small");
+        std::copy(ws->plan.advances.begin(), ws->plan.advances.end(), out);
+    });
+}
+
+uint64_t sn_workspace_allocation_events(const sn_workspace* ws) { return ws ? ws->alloc_events : 0; }
+uint64_t sn_workspace_last_launches(const sn_workspace* ws) { return ws ? ws->last_launches : 0; }
+
+sn_status sn_workspace_table(const sn_workspace* ws, int32_t table, double* out, uint64_t capacity,
+                             uint64_t* n_out) {
+    return guarded([&] {
+        if (!ws) argument_error("null argument");
+        const std::vector<double>* v = nullptr;
+        switch (table) {
+            case SN_TABLE_DEMOD_TAPS_REV: v = &ws->plan.demod_rev; break;
+            case SN_TABLE_DEMOD_LUT: v = &ws->plan.demod_lut; break;
+            case SN_TABLE_PREMF_TAPS_REV: v = &ws->plan.premf_rev; break;
+            case SN_TABLE_CHIRP_REF: v = &ws->plan.chirp_ref; break;
+            case SN_TABLE_SMOOTH_REV: v = &ws->plan.comp_rev; break;
+            default: argument_error("unknown table");
+        }
+        if (n_out) *n_out = v->size();
+        if (!out) return;
+        if (capacity < v->size()) argument_error("buffer too small");
+        std::copy(v->begin(), v->end(), out);
+    });
+}
+
+sn_status sn_workspace_stage(sn_workspace* ws, int32_t stage, uint64_t item, double* out,
+                             uint64_t capacity) {
+    return guarded([&] {
+        if (!ws || !out) argument_error("null argument");
+        ws->require_device();
+        if (item >= ws->max_batch) argument_error("item out of range");
+        const Sizes& z = ws->plan.sz;
+        const double* src = nullptr;
+        uint64_t n = 0;
+        switch (stage) {
+            case SN_STAGE_DEMOD: src = ws->d_demod + item * kCh * z.demod_len; n = kCh * z.demod_len; break;
+            case SN_STAGE_PREMF: src = ws->d_mf + item * kCh * z.mf_len; n = kCh * z.mf_len; break;
+            case SN_STAGE_FILT: src = ws->d_filt + item * kCh * z.mf_len; n = kCh * z.mf_len; break;
+            default: argument_error("unknown stage");
+        }
+        if (capacity < n) argument_error("buffer too small");
+        DeviceGuard g(ws->device);
+        ck(cudaStreamSynchronize(ws->stream), "sync");
+        ck(cudaMemcpy(out, src, n * sizeof(double), cudaMemcpyDeviceToHost), "stage copy");
+    });
+}
+
+sn_status sn_workspace_beamform(sn_workspace* ws, const double* filtered, uint64_t channels,
+                                uint64_t samples, double* out) {
+    return guarded([&] {
+        if (!ws || !filtered || !out) argument_error("null argument");
+        const Sizes& z = ws->plan.sz;
+        // pipeline.cpp:576-591 argument checks
+        if (channels != static_cast<uint64_t>(kCh)) {
+            argument_error("beamform: expected 32 channels, got " + std::to_string(channels));
+        }
+        if (samples != z.mf_len) {
+            argument_error("beamform: expected " + std::to_string(z.mf_len) +
+                           " samples per channel, got " + std::to_string(samples));
+        }
+        ws->require_device();
+        DeviceGuard g(ws->device);
+        const uint64_t L = z.mf_len;
+        double *d_in = nullptr, *d_out = nullptr;
+        ck(cudaMalloc(&d_in, kCh * L * sizeof(double)), "cudaMalloc");
+        ck(cudaMalloc(&d_out, z.n_dirs * L * sizeof(double)), "cudaMalloc");
+        cudaError_t e = cudaMemcpyAsync(d_in, filtered, kCh * L * sizeof(double), cudaMemcpyHostToDevice, ws->stream);
+        if (e == cudaSuccess) {
+            launch_beamform(d_in, d_out, ws->d_shifts, (int64_t)L, (int64_t)z.n_dirs, ws->stream);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_out, z.n_dirs * L * sizeof(double), cudaMemcpyDeviceToHost, ws->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ws->stream);
+        cudaFree(d_in);
+        cudaFree(d_out);
+        ck(e, "beamform");
+    });
+}
+
+} // extern "C"
