@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""Benchmark of the eRTIS image-formation hot path (Workspace::process).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Metric (BASELINE.json): energyscapes/s, 32-mic, 3D hemisphere grid
+(hemisphere3000, 3000 directions x 655 range bins, 5 m window = 144,800 PDM
+frames per capture) — BASELINE.json configs[1]. A "step" is one pass of the
+hot path over a batch of B captures per GPU; `value` = captures processed by
+all ranks / max-over-ranks device time (CUDA events on the launching stream).
+Inputs cycle through a pool of distinct synthetic captures whose total size
+exceeds the 126 MB L2, so no step re-reads cached inputs.
+
+Extra keys: `e2e` (same metric through the public host API with pinned host
+buffers: H2D of every capture + D2H of every energyscape inside the timed
+region), `latency_ms` (single-capture p50/p99), `roofline` (dominant kernel
+k_directions, algorithmic FLOPs per SURVEY.md §8(d) / its CUDA-event
+duration, against the FP64 FMA peak measured live on this GPU),
+`cpu_baseline` (the unmodified reference C++ core, oracle/_ref, on all host
+cores, rank 0 at N=1 only), `clocks`, `gpu_launches`.
+
+Multi-GPU (torchrun): one sensor per rank (serial = rank+1), no data-path
+collective (scaling "weak"); --gather adds the NCCL 360-degree energyscape
+gather to rank 0 inside each step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "energyscapes/sec (32-mic, 3D grid) at 1/2/4/8 B200 + p50 latency vs CPU ref"
+UNIT = "energyscapes/s"
+BENCH_SCENE = [(1.5, 0.2, 0.0, 0.8), (3.0, -0.4, 0.1, 0.5)]  # bench.cpp:113-117
+GRIDS = {"horizontal90": 0, "box1850": 1, "hemisphere3000": 2, "az181": 3}
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--grid", choices=list(GRIDS), default="hemisphere3000")
+    p.add_argument("--batch", type=int, default=16, help="captures per step per GPU")
+    p.add_argument("--pool", type=int, default=256, help="distinct captures per GPU")
+    p.add_argument("--precision", choices=["f64", "f32"], default="f64")
+    p.add_argument("--gather", action="store_true", help="NCCL 360-degree gather per step")
+    p.add_argument("--latency-samples", type=int, default=50)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-calls", type=int, default=2, help="reference calls per host thread")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def flops_per_energyscape(d):
+    """Algorithmic FLOPs (SURVEY.md §8(d) conventions: MAC=2, add=1, real FFT
+    of N = 2.5 N log2 N, complex multiply = 6, sqrt = 1)."""
+    import math
+    L, N, bins, comp = d["mf_samples"], d["env_fft_size"], d["range_bins"], d["smoothing_len"]
+    Nm, ref = d["mf_fft_size"], d["ref_len"]
+    demod = 32 * d["demod_samples"] * 255 * 2
+    premf = 32 * L * 65 * 2
+    mf = 32 * (2 * 2.5 * Nm * math.log2(Nm) + 6 * (Nm // 2 + 1))
+    per_dir = (32 * L + L) + 2 * 2.5 * N * math.log2(N) + 4 * L + bins * comp * 2
+    return demod + premf + mf, per_dir
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_config(sn, grid, precision):
+    if grid == "az181":
+        az = np.deg2rad(np.arange(-90, 91, dtype=np.float64))
+        cfg = sn.default_pipeline_config(sn.GridKind.horizontal90)
+        cfg = cfg.copy(directions=np.stack([az, np.zeros_like(az)], 1), grid_kind=3)
+    else:
+        cfg = sn.default_pipeline_config(GRIDS[grid])
+    return cfg.copy(precision=0 if precision == "f64" else 1)
+
+
+def synth_pool(sn, cfg, serial, n):
+    """n distinct captures (seed = 7 + 1000*serial + seq)."""
+    def one(seq):
+        scene = sn.Scene([sn.Reflector(*r) for r in BENCH_SCENE], 0.01, 7 + 1000 * serial + seq)
+        return sn.synthesize_measurement(cfg, scene, serial, seq * 100000, seq).packed
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        return np.stack(list(ex.map(one, range(n))))
+
+
+def workload_desc(grid, d, B, pool):
+    return {
+        "workload": (f"1 eRTIS sensor per GPU, 32 mics, {grid} ({d['n_directions']} directions x "
+                     f"{d['range_bins']} range bins), 5 m window = {d['frames']} PDM frames/capture"),
+        "grid": grid, "n_directions": d["n_directions"], "range_bins": d["range_bins"],
+        "frames": d["frames"], "batch_per_gpu": B, "pool_per_gpu": pool,
+        "l2_policy": f"inputs cycle through {pool} distinct captures "
+                     f"({pool * d['frames'] * 4 / 1e6:.0f} MB > 126 MB L2)",
+    }
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline(cfg_b200, grid, calls):
+    """Reference C++ core (oracle/_ref, reference Release flags) on all host
+    threads: one Workspace per thread, processing_threads=1 (central-node
+    model, central_node.cpp:48-53)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    ref = po.Ref(fast=True)
+    kind = 0 if grid == "az181" else GRIDS[grid]
+    rc = ref.default_config(kind)
+    if grid == "az181":
+        rc = rc.copy(directions=po.az181_directions(), grid_kind=3)
+    rc = rc.copy(processing_threads=1)
+    pool = np.stack([ref.synthesize(rc, BENCH_SCENE, 0.01, 7 + s) for s in range(4)])
+    threads = os.cpu_count() or 1
+    elapsed, total = ref.throughput(rc, pool, threads, calls)
+    return {
+        "value": total / elapsed, "unit": UNIT, "cores": threads, "kind": "reference",
+        "sample": (f"{total} process() calls of {grid} ({threads} threads x {calls}; "
+                   f"unmodified reference core built -O3 -march=x86-64-v3, FFT = test-only "
+                   f"FFTW-API shim; {elapsed:.2f} s wall)"),
+    }
+
+
+def run_reference(args):
+    """Reference arm: the reference's own CPU implementation (oracle/_ref,
+    unmodified core sources) on all host threads of this box. One step = every
+    host thread runs one process() call on its own Workspace; K is capped at
+    30 steps so the arm stays within a few minutes at hemisphere3000."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    steps = max(1, min(args.steps, 30))
+    base = cpu_baseline(None, args.grid, steps)
+    threads = base["cores"]
+    line = {
+        "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": 1,
+        "ms_per_step": 1e3 * threads / base["value"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference synthesize_measurement, bench scene, seeds 7..10)",
+        "config": {"workload": f"1 eRTIS sensor, 32 mics, {args.grid}, 5 m window = 144800 PDM "
+                               f"frames/capture; reference CPU path, {threads} workers x 1 thread",
+                   "grid": args.grid},
+        "impl": "reference", "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_b200(args):
+    import torch
+    import paper_2208_10839_b200 as sn
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    cfg = make_config(sn, args.grid, args.precision)
+    B = args.batch
+    pool_n = max(B, (args.pool // B) * B)
+    ws = sn.Workspace(cfg, device=local, max_batch=B)
+    d = ws.dims
+    serial = rank + 1
+    pool_h = synth_pool(sn, cfg, serial, pool_n)
+    pool = torch.from_numpy(pool_h).to(dev)
+    out = torch.empty((B, ws.n_dirs, ws.bins), dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    sptr = stream.cuda_stream
+    nchunks = pool_n // B
+
+    def step(k):
+        src = pool[(k % nchunks) * B]
+        ws.process_device(src.data_ptr(), B, out.data_ptr(), sptr)
+
+    gather_buf = None
+    if dist is not None and args.gather:
+        gather_buf = [torch.empty_like(out) for _ in range(world)] if rank == 0 else None
+
+    def gather():
+        if dist is not None and args.gather:
+            with torch.cuda.stream(stream):
+                dist.gather(out, gather_buf if rank == 0 else None, dst=0)
+
+    # ---- warm-up ----------------------------------------------------------
+    with torch.cuda.stream(stream):
+        for k in range(args.warmup):
+            step(k)
+            gather()
+    torch.cuda.synchronize(dev)
+
+    # ---- device-resident timed region ---------------------------------------
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for k in range(args.steps):
+                step(k)
+                gather()
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    elapsed_ms = e0.elapsed_time(e1)
+    launches = ws.last_launches() * args.steps
+    if dist is not None:
+        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    value = world * args.steps * B / (elapsed_ms / 1e3)
+
+    # ---- e2e through the public host API (pinned buffers) ---------------------
+    pin_in = torch.from_numpy(pool_h[: 2 * B]).pin_memory()
+    pin_out = torch.empty((B, ws.n_dirs, ws.bins), dtype=torch.float32).pin_memory()
+    pin_in_np, pin_out_np = pin_in.numpy(), pin_out.numpy()
+    for k in range(max(1, args.warmup)):
+        ws.process_packed_host(pin_in_np[(k % 2) * B:(k % 2 + 1) * B], pin_out_np)
+    if dist is not None:
+        dist.barrier()
+    e2e_steps = max(5, args.steps // 2)
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        ws.process_packed_host(pin_in_np[(k % 2) * B:(k % 2 + 1) * B], pin_out_np)
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * e2e_steps * B / e2e_s
+
+    # ---- single-capture latency (host API, 1 capture) -------------------------
+    lat = []
+    m = sn.RawMeasurement(serial, 0, 0, 32, ws.frames, cfg.pdm_rate, pool_h[0])
+    for i in range(args.latency_samples + 3):
+        t0 = time.perf_counter()
+        ws.process(m)
+        if i >= 3:
+            lat.append((time.perf_counter() - t0) * 1e3)
+    dev_lat = []
+    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        for i in range(args.latency_samples + 3):
+            ev_a.record(stream)
+            ws.process_device(pool[i % pool_n].data_ptr(), 1, out.data_ptr(), sptr)
+            ev_b.record(stream)
+            ev_b.synchronize()
+            if i >= 3:
+                dev_lat.append(ev_a.elapsed_time(ev_b))
+
+    # ---- per-kernel timing for the roofline (separate pass) --------------------
+    ws.set_profiling(True)
+    stage_ms = {"demod": [], "premf": [], "matched_filter": [], "directions": []}
+    with torch.cuda.stream(stream):
+        for k in range(min(20, args.steps)):
+            step(k)
+            stream.synchronize()
+            for kk, v in ws.stage_times().items():
+                stage_ms[kk].append(v)
+    ws.set_profiling(False)
+    stage_avg = {k: float(np.mean(v)) for k, v in stage_ms.items()}
+    fe_flops, dir_flops = flops_per_energyscape(d)
+    peak64 = sn.measure_fp_peak(local, sn.Precision.f64 if args.precision == "f64" else sn.Precision.f32)
+    dir_flops_launch = dir_flops * d["n_directions"] * B
+    achieved = dir_flops_launch / (stage_avg["directions"] * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            key = f"{args.grid}/{args.precision}/B{B}"
+            traffic = tj.get(key)
+        except Exception:
+            traffic = None
+    total_step_ms = sum(stage_avg.values())
+    bytes_per = 32 * d["frames"] // 8 + 4 * d["n_directions"] * d["range_bins"]
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
+        "data": "synthetic (product synthesize_measurement, bench scene bench.cpp:113-117, "
+                "seeds 7+1000*serial+seq)",
+        "config": {**workload_desc(args.grid, d, B, pool_n), "precision": args.precision,
+                   "parallelism": f"{world} GPU(s), one sensor per GPU, no data-path collective"
+                                  + (", NCCL gather to rank 0" if args.gather else "")},
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": B * 32 * d["frames"] // 8,
+                "d2h_bytes_per_step": B * 4 * d["n_directions"] * d["range_bins"],
+                "api": "Workspace.process_packed_host (sn_workspace_process_batch), pinned buffers"},
+        "latency_ms": {
+            "p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
+            "device_p50": float(np.percentile(dev_lat, 50)),
+            "device_p99": float(np.percentile(dev_lat, 99)),
+            "what": "1 capture: host API incl. H2D+D2H (p50/p99); device-only (device_*)"},
+        "roofline": {
+            "kernel": "k_directions (beamform + Hilbert FFT pair + |.| + 447-tap FIR /10)",
+            "bound": args.precision, "achieved": achieved, "peak": peak64, "unit": "TFLOP/s",
+            "frac": achieved / peak64, "traffic": traffic,
+            "peak_source": "measured live: FMA-chain microbenchmark (sn_measure_fp_peak) on this GPU; "
+                           "MEASURED_PEAKS.json has no CUDA-core figure",
+            "flops_per_launch": dir_flops_launch, "kernel_ms": stage_avg["directions"],
+            "share_of_step": stage_avg["directions"] / total_step_ms if total_step_ms else None,
+            "stage_ms": stage_avg,
+            "whole_path_tflops": (fe_flops + dir_flops * d["n_directions"]) * value / world / 1e12,
+            "hbm_compulsory_gbs": bytes_per * value / world / 1e9,
+        },
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg, args.grid, args.cpu_calls)
+        except Exception as e:  # the GPU number stands on its own
+            line["cpu_baseline"] = {"error": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

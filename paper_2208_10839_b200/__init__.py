@@ -169,6 +169,9 @@ def lib() -> C.CDLL:
     L.sn_workspace_last_launches.restype = u64
     L.sn_workspace_table.argtypes = [vp, i32, vp, u64, C.POINTER(u64)]
     L.sn_workspace_stage.argtypes = [vp, i32, u64, vp, u64]
+    L.sn_workspace_set_profiling.argtypes = [vp, C.c_int]
+    L.sn_workspace_stage_times.argtypes = [vp, vp]
+    L.sn_measure_fp_peak.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
     _lib = L
     return L
 
@@ -177,6 +180,13 @@ def _check(rc: int):
     if rc != 0:
         msg = lib().sn_last_error().decode(errors="replace")
         raise _ERRORS.get(rc, SonarError)(msg)
+
+
+def measure_fp_peak(device: int = 0, precision: Precision = Precision.f64) -> float:
+    """FMA throughput of the CUDA cores in TFLOP/s (FMA = 2 flops)."""
+    v = C.c_double(0)
+    _check(lib().sn_measure_fp_peak(device, int(precision), C.byref(v)))
+    return v.value
 
 
 # ---------------------------------------------------------------------------
@@ -452,6 +462,15 @@ class Workspace:
         out = np.empty(n.value, np.float64)
         _check(lib().sn_workspace_table(self._h, which, out.ctypes.data, n.value, C.byref(n)))
         return out
+
+    def set_profiling(self, enable: bool = True):
+        _check(lib().sn_workspace_set_profiling(self._h, int(enable)))
+
+    def stage_times(self) -> dict:
+        """Device ms of {demod, premf, matched_filter, directions} of the last call."""
+        out = np.zeros(4, np.float32)
+        _check(lib().sn_workspace_stage_times(self._h, out.ctypes.data))
+        return dict(zip(("demod", "premf", "matched_filter", "directions"), map(float, out)))
 
     def stage(self, which: int, item: int = 0) -> np.ndarray:
         L = self.dims["demod_samples"] if which == 0 else self.dims["mf_samples"]

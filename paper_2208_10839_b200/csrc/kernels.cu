@@ -298,6 +298,53 @@ void launch_beamform(const double* filt, double* beams, const int32_t* shifts, i
         filt, beams, shifts, L);
 }
 
+// FMA-throughput microbenchmark (roofline denominator for the CUDA-core
+// stages: MEASURED_PEAKS.json carries only HBM and bf16 tensor figures).
+// 8 independent FMA chains per thread, 4 x 148 CTAs x 256 threads.
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_fma_peak(R* out, int iters, R seed) {
+    R a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = seed + (R)(threadIdx.x + i);
+    const R m = (R)0.999999, c = (R)1e-7;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = fma(a[i], m, c);
+        }
+    }
+    R s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += a[i];
+    if (s == (R)12345.678) out[threadIdx.x] = s; // keep the chains live
+}
+
+double measure_fma_peak(int sms, bool f32) {
+    void* out = nullptr;
+    cudaMalloc(&out, kThreads * 8);
+    const int blocks = sms * 4, iters = 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(e0);
+        if (f32) k_fma_peak<float><<<blocks, kThreads>>>((float*)out, iters, 1.0f);
+        else k_fma_peak<double><<<blocks, kThreads>>>((double*)out, iters, 1.0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0) best = ms < best ? ms : best;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    const double flops = 2.0 * 8 * 16 * (double)iters * kThreads * blocks;
+    return flops / (best * 1e-3) / 1e12;
+}
+
 // ---------------------------------------------------------------------------
 size_t demod_smem_bytes(int octets, int words) {
     return (size_t)octets * 256 * sizeof(double) + (size_t)32 * words * sizeof(uint32_t);

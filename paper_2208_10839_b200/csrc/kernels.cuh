@@ -73,6 +73,8 @@ void launch_rfft_forward(const double* x, double2* X, const double2* tw, int n, 
 void launch_beamform(const double* filt, double* beams, const int32_t* shifts, int64_t L,
                      int64_t n_dirs, cudaStream_t s);
 
+double measure_fma_peak(int sms, bool f32);
+
 size_t demod_smem_bytes(int octets, int words);
 size_t fft_smem_bytes(int n, int real_bytes);
 

@@ -116,6 +116,9 @@ struct sn_workspace {
     int dir_grid = 0;
     uint64_t packed_bytes = 0, energy_per = 0;
     uint64_t alloc_events = 0, device_allocs = 0, last_launches = 0;
+    // optional per-stage timing (events on the launching stream)
+    bool profiling = false;
+    cudaEvent_t ev[5] = {};
     // graph cache
     cudaGraphExec_t graph = nullptr;
     const uint8_t* g_in = nullptr;
@@ -128,6 +131,9 @@ struct sn_workspace {
         cudaGetDevice(&prev);
         cudaSetDevice(device);
         if (graph) cudaGraphExecDestroy(graph);
+        for (cudaEvent_t e : ev) {
+            if (e) cudaEventDestroy(e);
+        }
         for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
                         (void*)d_filt32, (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
@@ -173,6 +179,7 @@ struct sn_workspace {
         d_tw_env = dmalloc<double2>(s.env_fft, n);
         d_tw_env32 = dmalloc<float2>(s.env_fft, n);
         ck(cudaMallocHost(&h_in, B * packed_bytes), "cudaMallocHost");
+        for (cudaEvent_t& e : ev) ck(cudaEventCreate(&e), "cudaEventCreate");
         ck(cudaMallocHost(&h_out, B * energy_per * sizeof(float)), "cudaMallocHost");
 
         upload(d_lut, plan.demod_lut, stream);
@@ -247,13 +254,17 @@ struct sn_workspace {
         da.packed = d_in;
         da.demod = d_demod;
         da.batch = (int)count;
+        if (profiling) cudaEventRecord(ev[0], s);
         launch_demod(da, demod_grid, demod_smem, s);
+        if (profiling) cudaEventRecord(ev[1], s);
         PremfArgs pa{d_demod, d_mf, d_premf, (int64_t)z.demod_len, (int64_t)z.mf_len,
                      (int)plan.premf_rev.size(), plan.cfg.pre_mf_decimation};
         launch_premf(pa, (int)count, s);
+        if (profiling) cudaEventRecord(ev[2], s);
         MfArgs ma{d_mf, d_filt, f32 ? d_filt32 : nullptr, d_ref_spec, d_tw_mf,
                   (int64_t)z.mf_len, (int)z.mf_fft, (int)z.ref_len};
         launch_matched_filter(ma, (int)count, mf_smem, s);
+        if (profiling) cudaEventRecord(ev[3], s);
         DirArgs ra{};
         ra.filt = f32 ? (const void*)d_filt32 : (const void*)d_filt;
         ra.energy = d_out;
@@ -270,6 +281,7 @@ struct sn_workspace {
         const int grid = (int)std::min<int64_t>(dir_grid, (int64_t)(z.n_dirs * count));
         if (f32) launch_directions_f32(ra, grid, dir_smem, s);
         else launch_directions_f64(ra, grid, dir_smem, s);
+        if (profiling) cudaEventRecord(ev[4], s);
         ck(cudaGetLastError(), "kernel launch");
         last_launches = 4;
     }
@@ -295,22 +307,44 @@ struct sn_workspace {
         }
     }
 
+    static bool is_pinned(const void* p) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    }
+
+    // Host path: H2D of every capture, the device pipeline, D2H of the
+    // energyscapes, one stream synchronisation. Caller buffers that are
+    // page-locked are DMA'd directly; pageable ones go through the
+    // workspace's pinned staging buffers.
     void process_host(const sn_raw_measurement* ms, uint64_t count, float* out) {
         require_device();
         for (uint64_t i = 0; i < count; ++i) validate(ms[i]); // all-or-error
         DeviceGuard g(device);
+        const bool out_pinned = is_pinned(out);
         uint64_t done = 0;
         while (done < count) {
             const uint64_t c = std::min(max_batch, count - done);
             for (uint64_t i = 0; i < c; ++i) {
-                std::memcpy(h_in + i * packed_bytes, ms[done + i].packed, packed_bytes);
+                const uint8_t* src = ms[done + i].packed;
+                if (is_pinned(src)) {
+                    ck(cudaMemcpyAsync(d_packed + i * packed_bytes, src, packed_bytes,
+                                       cudaMemcpyHostToDevice, stream), "H2D");
+                } else {
+                    std::memcpy(h_in + i * packed_bytes, src, packed_bytes);
+                    ck(cudaMemcpyAsync(d_packed + i * packed_bytes, h_in + i * packed_bytes,
+                                       packed_bytes, cudaMemcpyHostToDevice, stream), "H2D");
+                }
             }
-            ck(cudaMemcpyAsync(d_packed, h_in, c * packed_bytes, cudaMemcpyHostToDevice, stream), "H2D");
             enqueue(d_packed, c, d_energy, stream);
-            ck(cudaMemcpyAsync(h_out, d_energy, c * energy_per * sizeof(float), cudaMemcpyDeviceToHost,
+            float* dst = out_pinned ? out + done * energy_per : h_out;
+            ck(cudaMemcpyAsync(dst, d_energy, c * energy_per * sizeof(float), cudaMemcpyDeviceToHost,
                                stream), "D2H");
             ck(cudaStreamSynchronize(stream), "process sync");
-            std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
+            if (!out_pinned) std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
             done += c;
         }
     }
@@ -570,6 +604,34 @@ sn_status sn_workspace_beamform(sn_workspace* ws, const double* filtered, uint64
         cudaFree(d_in);
         cudaFree(d_out);
         ck(e, "beamform");
+    });
+}
+
+sn_status sn_workspace_set_profiling(sn_workspace* ws, int enable) {
+    return guarded([&] {
+        if (!ws) argument_error("null argument");
+        ws->profiling = enable != 0;
+    });
+}
+
+sn_status sn_workspace_stage_times(sn_workspace* ws, float* ms4) {
+    return guarded([&] {
+        if (!ws || !ms4) argument_error("null argument");
+        ws->require_device();
+        if (!ws->profiling) argument_error("profiling is not enabled");
+        DeviceGuard g(ws->device);
+        ck(cudaEventSynchronize(ws->ev[4]), "event sync");
+        for (int i = 0; i < 4; ++i) ck(cudaEventElapsedTime(&ms4[i], ws->ev[i], ws->ev[i + 1]), "elapsed");
+    });
+}
+
+sn_status sn_measure_fp_peak(int device, int precision, double* tflops) {
+    return guarded([&] {
+        if (!tflops) argument_error("null argument");
+        DeviceGuard g(device);
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        *tflops = measure_fma_peak(sms, precision == SN_PRECISION_F32);
     });
 }
 
