@@ -76,6 +76,20 @@ def flops_per_energyscape(d):
     return demod + premf + mf, per_dir
 
 
+def kernel_flops(d):
+    """Algorithmic FLOPs per energyscape for each device kernel."""
+    import math
+    L, N, bins, comp = d["mf_samples"], d["env_fft_size"], d["range_bins"], d["smoothing_len"]
+    Nm, n = d["mf_fft_size"], d["n_directions"]
+    return {
+        "demod": 32 * d["demod_samples"] * 255 * 2,
+        "premf": 32 * L * 65 * 2,
+        "matched_filter": 32 * (2 * 2.5 * Nm * math.log2(Nm) + 6 * (Nm // 2 + 1)),
+        "beamform": n * (32 * L + L),
+        "envelope": n * (2 * 2.5 * N * math.log2(N) + 4 * L + bins * comp * 2),
+    }
+
+
 class ClockSampler:
     """NVML sampling of SM clock + throttle reasons during the timed region."""
     REASONS = {
@@ -327,7 +341,7 @@ def run_b200(args):
 
     # ---- per-kernel timing for the roofline (separate pass) --------------------
     ws.set_profiling(True)
-    stage_ms = {"demod": [], "premf": [], "matched_filter": [], "directions": []}
+    stage_ms = {k: [] for k in sn.STAGES}
     with torch.cuda.stream(stream):
         for k in range(min(20, args.steps)):
             step(k)
@@ -337,16 +351,19 @@ def run_b200(args):
     ws.set_profiling(False)
     stage_avg = {k: float(np.mean(v)) for k, v in stage_ms.items()}
     fe_flops, dir_flops = flops_per_energyscape(d)
-    peak64 = sn.measure_fp_peak(local, sn.Precision.f64 if args.precision == "f64" else sn.Precision.f32)
-    dir_flops_launch = dir_flops * d["n_directions"] * B
-    achieved = dir_flops_launch / (stage_avg["directions"] * 1e-3) / 1e12
+    peak = sn.measure_fp_peak(local, sn.Precision.f64 if args.precision == "f64" else sn.Precision.f32)
+    kflops = kernel_flops(d)  # per energyscape, SURVEY.md §8(d) rows
+    kernels = {}
+    for k, ms in stage_avg.items():
+        f = kflops[k] * B
+        kernels[k] = {"ms": ms, "tflops": f / (ms * 1e-3) / 1e12,
+                      "frac": f / (ms * 1e-3) / 1e12 / peak}
+    dom = max(stage_avg, key=stage_avg.get)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            tj = json.load(open(tpath))
-            key = f"{args.grid}/{args.precision}/B{B}"
-            traffic = tj.get(key)
+            traffic = json.load(open(tpath)).get(f"{args.grid}/{args.precision}/B{B}/{dom}")
         except Exception:
             traffic = None
     total_step_ms = sum(stage_avg.values())
@@ -371,14 +388,13 @@ def run_b200(args):
             "device_p99": float(np.percentile(dev_lat, 99)),
             "what": "1 capture: host API incl. H2D+D2H (p50/p99); device-only (device_*)"},
         "roofline": {
-            "kernel": "k_directions (beamform + Hilbert FFT pair + |.| + 447-tap FIR /10)",
-            "bound": args.precision, "achieved": achieved, "peak": peak64, "unit": "TFLOP/s",
-            "frac": achieved / peak64, "traffic": traffic,
-            "peak_source": "measured live: FMA-chain microbenchmark (sn_measure_fp_peak) on this GPU; "
-                           "MEASURED_PEAKS.json has no CUDA-core figure",
-            "flops_per_launch": dir_flops_launch, "kernel_ms": stage_avg["directions"],
-            "share_of_step": stage_avg["directions"] / total_step_ms if total_step_ms else None,
-            "stage_ms": stage_avg,
+            "kernel": dom, "bound": args.precision, "achieved": kernels[dom]["tflops"],
+            "peak": peak, "unit": "TFLOP/s", "frac": kernels[dom]["frac"], "traffic": traffic,
+            "peak_source": "measured live: FMA-chain microbenchmark (sn_measure_fp_peak) on this "
+                           "GPU; MEASURED_PEAKS.json has no CUDA-core FP64/FP32 figure",
+            "flops_per_launch": kflops[dom] * B, "kernel_ms": stage_avg[dom],
+            "share_of_step": stage_avg[dom] / total_step_ms if total_step_ms else None,
+            "kernels": kernels,
             "whole_path_tflops": (fe_flops + dir_flops * d["n_directions"]) * value / world / 1e12,
             "hbm_compulsory_gbs": bytes_per * value / world / 1e9,
         },
@@ -397,6 +413,7 @@ def run_b200(args):
     return 0
 
 
+# ---------------------------------------------------------------------------
 def main():
     args = parse_args()
     if args.impl == "reference":

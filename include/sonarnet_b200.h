@@ -225,9 +225,10 @@ sn_status sn_workspace_process_device_graph(sn_workspace* ws, const uint8_t* d_p
 
 /* Per-stage device timing of the next process calls (CUDA events on the
  * launching stream). stage_times: ms for {demod, premf, matched filter,
- * directions} of the most recent call. Diagnostics for the roofline report. */
+ * beamform, envelope} of the most recent call. Diagnostics for the roofline
+ * report. */
 sn_status sn_workspace_set_profiling(sn_workspace* ws, int enable);
-sn_status sn_workspace_stage_times(sn_workspace* ws, float* ms4);
+sn_status sn_workspace_stage_times(sn_workspace* ws, float* ms5);
 
 /* FMA-throughput microbenchmark on `device` (TFLOP/s, FMA = 2 flops); the
  * roofline denominator for CUDA-core kernels (no tensor cores involved). */

@@ -136,6 +136,8 @@ class _Scene(C.Structure):
 
 _lib: Optional[C.CDLL] = None
 
+STAGES = ("demod", "premf", "matched_filter", "beamform", "envelope")
+
 
 def lib() -> C.CDLL:
     """Load libsonarnet_b200.so (raises if it was not built — no fallback)."""
@@ -467,10 +469,10 @@ class Workspace:
         _check(lib().sn_workspace_set_profiling(self._h, int(enable)))
 
     def stage_times(self) -> dict:
-        """Device ms of {demod, premf, matched_filter, directions} of the last call."""
-        out = np.zeros(4, np.float32)
+        """Device ms of {demod, premf, matched_filter, beamform, envelope} of the last call."""
+        out = np.zeros(5, np.float32)
         _check(lib().sn_workspace_stage_times(self._h, out.ctypes.data))
-        return dict(zip(("demod", "premf", "matched_filter", "directions"), map(float, out)))
+        return dict(zip(STAGES, map(float, out)))
 
     def stage(self, which: int, item: int = 0) -> np.ndarray:
         L = self.dims["demod_samples"] if which == 0 else self.dims["mf_samples"]

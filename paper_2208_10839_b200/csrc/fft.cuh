@@ -23,6 +23,16 @@ template <> struct Cx<float> { using T = float2; };
 
 __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
 
+// Thread groups: a CTA may run several independent 256-thread groups, each on
+// its own work item and shared-memory region; FFT phases synchronise with a
+// per-group named barrier (id 1 + group) instead of __syncthreads.
+constexpr int kGroupThreads = 256;
+__device__ __forceinline__ int gtid() { return threadIdx.x & (kGroupThreads - 1); }
+__device__ __forceinline__ int gidx() { return threadIdx.x / kGroupThreads; }
+__device__ __forceinline__ void gsync() {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + gidx()), "r"(kGroupThreads) : "memory");
+}
+
 template <typename V> __device__ __forceinline__ V cadd(V a, V b) { return {a.x + b.x, a.y + b.y}; }
 template <typename V> __device__ __forceinline__ V csub(V a, V b) { return {a.x - b.x, a.y - b.y}; }
 template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
@@ -136,7 +146,7 @@ template <int RADIX, bool INV, bool SRC_PADDED, typename V>
 __device__ __forceinline__ void stockham_pass(const V* src, V* dst, int M, int ns,
                                               const V* __restrict__ tw, int tws) {
     const int nj = M / RADIX;
-    const int j = threadIdx.x;
+    const int j = gtid();
     V v[RADIX];
     const bool active = j < nj;
     if (active) {
@@ -157,41 +167,27 @@ __device__ __forceinline__ void stockham_pass(const V* src, V* dst, int M, int n
         }
         dft_r<RADIX, INV>(v);
     }
-    __syncthreads();
+    gsync();
     if (active) {
         const int k = j % ns;
         const int base = (j / ns) * ns * RADIX + k;
 #pragma unroll
         for (int r = 0; r < RADIX; ++r) dst[pad16(base + out_slot<RADIX>(r) * ns)] = v[r];
     }
-    __syncthreads();
+    gsync();
 }
 
-// Full M-point complex FFT (M = 2^m, 16 <= M <= 16*blockDim). The first pass
-// reads `src` (padded or not), all later passes work in place on `buf`.
-template <bool INV, bool SRC_PADDED, typename V>
-__device__ void cfft(const V* src, V* buf, int M, const V* __restrict__ tw, int tws) {
-    int ns = 1;
-    bool first = true;
-    int rem = M;
-    while (rem >= 16) {
-        if (first) stockham_pass<16, INV, SRC_PADDED>(src, buf, M, ns, tw, tws);
-        else stockham_pass<16, INV, true>(buf, buf, M, ns, tw, tws);
-        first = false;
-        ns *= 16;
-        rem /= 16;
-    }
-    if (rem > 1) {
-        if (rem == 8) {
-            if (first) stockham_pass<8, INV, SRC_PADDED>(src, buf, M, ns, tw, tws);
-            else stockham_pass<8, INV, true>(buf, buf, M, ns, tw, tws);
-        } else if (rem == 4) {
-            if (first) stockham_pass<4, INV, SRC_PADDED>(src, buf, M, ns, tw, tws);
-            else stockham_pass<4, INV, true>(buf, buf, M, ns, tw, tws);
-        } else {
-            if (first) stockham_pass<2, INV, SRC_PADDED>(src, buf, M, ns, tw, tws);
-            else stockham_pass<2, INV, true>(buf, buf, M, ns, tw, tws);
-        }
+// Full M-point complex FFT, M a compile-time power of two in [16, 4096]:
+// radix-16 passes, then one radix-2/4/8 pass for the remaining factor. The
+// first pass reads `src` (padded or not); later passes work in place on `buf`.
+template <int M, bool INV, bool SRC_PADDED, int NS = 1, typename V>
+__device__ __forceinline__ void cfft(const V* src, V* buf, const V* __restrict__ tw, int tws) {
+    constexpr int REM = M / NS;
+    if constexpr (REM >= 16) {
+        stockham_pass<16, INV, SRC_PADDED>(src, buf, M, NS, tw, tws);
+        cfft<M, INV, true, NS * 16>(buf, buf, tw, tws);
+    } else if constexpr (REM > 1) {
+        stockham_pass<REM, INV, SRC_PADDED>(src, buf, M, NS, tw, tws);
     }
 }
 
@@ -205,7 +201,7 @@ __device__ void cfft(const V* src, V* buf, int M, const V* __restrict__ tw, int 
 template <typename V, typename Op>
 __device__ __forceinline__ void real_spectral_op(V* buf, int M, const V* __restrict__ twN, Op op) {
     using R = decltype(V{}.x);
-    for (int k = threadIdx.x; k <= M / 2; k += blockDim.x) {
+    for (int k = gtid(); k <= M / 2; k += kGroupThreads) {
         if (k == 0) {
             const V z0 = buf[0];
             const V x0 = {z0.x + z0.y, (R)0};
@@ -242,7 +238,7 @@ __device__ __forceinline__ void real_spectral_op(V* buf, int M, const V* __restr
             buf[pad16(kk)] = V{e3.x - o3.y, e3.y + o3.x};
         }
     }
-    __syncthreads();
+    gsync();
 }
 
 } // namespace snb

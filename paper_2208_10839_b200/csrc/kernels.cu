@@ -144,24 +144,26 @@ __global__ void __launch_bounds__(kThreads) k_premf(PremfArgs a) {
 // zero-padded row, product with the spectrum of the reversed chirp, inverse,
 // 1/N, and the window [ref_len-1, ref_len-1+mf_len) (pipeline.cpp:555-562).
 // ---------------------------------------------------------------------------
+template <int M>
 __global__ void __launch_bounds__(kThreads) k_matched_filter(MfArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int N = a.n, M = N / 2;
+    constexpr int N = 2 * M;
     double* bufA = reinterpret_cast<double*>(smem);
     double2* bufB = reinterpret_cast<double2*>(bufA + N);
     const size_t row = (size_t)blockIdx.y * 32 + blockIdx.x;
     const double* x = a.mf + row * a.mf_len;
     for (int i = threadIdx.x; i < N; i += blockDim.x) bufA[i] = i < a.mf_len ? x[i] : 0.0;
     __syncthreads();
-    cfft<false, false>(reinterpret_cast<const double2*>(bufA), bufB, M, a.tw, 2);
+    cfft<M, false, false>(reinterpret_cast<const double2*>(bufA), bufB, a.tw, 2);
     const double scale = 2.0 / (double)N;
     const double2* R = a.ref_spec;
     real_spectral_op(bufB, M, a.tw, [&](double2 X, int k) {
         return cmul(X, double2{R[k].x * scale, R[k].y * scale});
     });
-    cfft<true, true>(bufB, bufB, M, a.tw, 2);
-    double* out = a.filt + row * a.mf_len;
-    float* out32 = a.filt32 ? a.filt32 + row * a.mf_len : nullptr;
+    cfft<M, true, true>(bufB, bufB, a.tw, 2);
+    // padded rows: sample n at [row * Lp + H + n]; the halo stays zero
+    double* out = a.filt + row * a.Lp + a.H;
+    float* out32 = a.filt32 ? a.filt32 + row * a.Lp + a.H : nullptr;
     for (int64_t n = threadIdx.x; n < a.mf_len; n += blockDim.x) {
         const int64_t q = n + a.ref_len - 1;
         const double2 z = bufB[pad16((int)(q >> 1))];
@@ -172,15 +174,16 @@ __global__ void __launch_bounds__(kThreads) k_matched_filter(MfArgs a) {
 }
 
 // Forward real FFT of one length-n row (setup: spectrum of the reversed chirp).
+template <int M>
 __global__ void __launch_bounds__(kThreads) k_rfft_forward(const double* x, double2* X,
-                                                           const double2* tw, int N) {
+                                                           const double2* tw) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int M = N / 2;
+    constexpr int N = 2 * M;
     double* bufA = reinterpret_cast<double*>(smem);
     double2* bufB = reinterpret_cast<double2*>(bufA + N);
     for (int i = threadIdx.x; i < N; i += blockDim.x) bufA[i] = x[i];
     __syncthreads();
-    cfft<false, false>(reinterpret_cast<const double2*>(bufA), bufB, M, tw, 2);
+    cfft<M, false, false>(reinterpret_cast<const double2*>(bufA), bufB, tw, 2);
     for (int k = threadIdx.x; k <= M; k += blockDim.x) {
         const int k1 = k % M, k2 = (M - k) % M;
         const double2 zk = bufB[pad16(k1)], zkk = bufB[pad16(k2)];
@@ -192,85 +195,199 @@ __global__ void __launch_bounds__(kThreads) k_rfft_forward(const double* x, doub
 }
 
 // ---------------------------------------------------------------------------
-// k_directions<R>: one (measurement, direction) per iteration of a persistent
-// CTA: delay-and-sum (pipeline.cpp:432-446) into shared memory, Hilbert
-// transform via a real FFT pair with DC and Nyquist zeroed and X -> -iX
-// (pipeline.cpp:448-461), |x + iH(x)| (:462-464), the 447-tap composite
-// smoothing/anti-alias FIR at stride 10 (:466-468, filters.hpp:14-39) and the
-// clamp/float write-out (:469-471).
-// R = double reproduces the reference arithmetic (beam bit-exact, spectral
-// stages within FP64 rounding); R = float is the F32 mode.
+// Per-direction stage, split in two kernels joined by an HBM/L2 beam buffer.
+//
+// k_beamform_tiles<R>: delay-and-sum (pipeline.cpp:432-446) for 256
+// directions x T samples per CTA. The zero-haloed filt rows of one time tile
+// (32 channels x (T + 2H), H = max |shift|) are staged in shared memory once
+// and reused by all 256 directions; lane = direction. Directions are visited
+// in Morton order of their unit vectors (Plan::order), so the 32 lanes of a
+// warp need samples a few positions apart and each shared-memory load is
+// served by one or two wavefronts. Channels are accumulated in the
+// reference order 0..31 and scaled by 1/32 (exact), so the FP64 beam is
+// bit-identical to the reference's; the zero halo reproduces its zero-fill
+// (adding +0.0 to a partial sum that is never -0.0 is the identity).
 // ---------------------------------------------------------------------------
 template <typename R>
-__global__ void __launch_bounds__(kThreads) k_directions(DirArgs a) {
+__global__ void __launch_bounds__(kThreads) k_beamform_tiles(BeamArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    R* tile = reinterpret_cast<R*>(smem);
+    const int W = a.T + 2 * a.H;
+    const int64_t t0 = (int64_t)blockIdx.x * a.T;
+    const int b = blockIdx.z;
+    const R* fb = reinterpret_cast<const R*>(a.filt) + (size_t)b * 32 * a.Lp;
+    for (int idx = threadIdx.x; idx < 32 * W; idx += blockDim.x) {
+        const int i = idx / W, e = idx - i * W;
+        const int64_t g = t0 + e; // padded index: sample t0 - H + e
+        tile[idx] = g < a.Lp ? fb[(size_t)i * a.Lp + g] : (R)0;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t slot = ((int64_t)blockIdx.y * (kThreads / 32) + warp) * 32 + lane;
+    if (slot >= a.n_dirs) return;
+    int off[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) off[i] = i * W + a.H - a.shifts[slot * 32 + i];
+    const int nmax = (int)((a.L - t0) < a.T ? (a.L - t0) : (int64_t)a.T);
+    R* out = reinterpret_cast<R*>(a.beams) + ((size_t)b * a.n_dirs + slot) * a.N + t0;
+    const R scale = (R)(1.0 / 32.0);
+    for (int n = 0; n < nmax; n += 4) {
+        R c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const R* p = tile + off[i] + n;
+            c0 += p[0];
+            c1 += p[1];
+            c2 += p[2];
+            c3 += p[3];
+        }
+        if (n + 4 <= nmax) {
+            if constexpr (sizeof(R) == 8) {
+                reinterpret_cast<double2*>(out + n)[0] = double2{c0 * scale, c1 * scale};
+                reinterpret_cast<double2*>(out + n)[1] = double2{c2 * scale, c3 * scale};
+            } else {
+                *reinterpret_cast<float4*>(out + n) = float4{c0 * scale, c1 * scale, c2 * scale, c3 * scale};
+            }
+        } else {
+            const R v[4] = {c0, c1, c2, c3};
+            for (int k = 0; k < nmax - n; ++k) out[n + k] = v[k] * scale;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_envelope<R, G>: per (measurement, direction): Hilbert transform of the
+// beam via a real FFT pair with DC and Nyquist zeroed and X -> -iX
+// (pipeline.cpp:448-461), |b + iH(b)| (:462-464), the composite
+// smoothing/anti-alias FIR at stride D3 with the reference's clipped window
+// and four-lane order (:466-468, filters.hpp:14-39), clamp and f32 write
+// (:469-471). G independent 256-thread groups per CTA, each with its own
+// shared-memory FFT buffer and named barrier, so one group's barrier waits
+// overlap another group's work. The beam is read from global memory twice
+// (first FFT pass, magnitude) instead of being held in shared memory; the
+// envelope is written over the Hilbert output in place.
+// ---------------------------------------------------------------------------
+// Composite smoothing/anti-alias FIR evaluated at stride D (the work of
+// detail::strided_filter, filters.hpp:14-39, at pipeline.cpp:466-468), in
+// polyphase form: out[k] = sum_p sum_q rev[q*D + p] * e_p[k + q]. A thread
+// owns FIR_R consecutive outputs (odd, so a warp's loads of one phase row are
+// bank-conflict free); for each phase it slides a register window over e_p
+// with the q loop fully unrolled (Q = 45 for the reference's 447 taps / 10),
+// one shared load + one broadcast tap per FIR_R FMAs. Taps beyond comp_len
+// are zero (the tap array is zero-padded to Q*D).
+constexpr int FIR_R = 9;
+constexpr int FIR_Q = 45;
+
+template <typename R>
+__device__ __forceinline__ void fir_polyphase(const R* ph, const R* comp, const EnvArgs& a,
+                                              float* eo) {
+    const int tid = gtid();
+    const int groups = (int)((a.bins + FIR_R - 1) / FIR_R);
+    if (a.fir_q == FIR_Q) {
+        for (int g = tid; g < groups; g += kGroupThreads) {
+            const int k0 = g * FIR_R;
+            R acc[FIR_R];
+#pragma unroll
+            for (int r = 0; r < FIR_R; ++r) acc[r] = 0;
+            for (int p = 0; p < a.decim; ++p) {
+                const R* row = ph + p * a.phase_len + k0;
+                const R* tp = comp + p;
+                R w[FIR_R + FIR_Q];
+#pragma unroll
+                for (int r = 0; r < FIR_R; ++r) w[r] = row[r];
+#pragma unroll
+                for (int q = 0; q < FIR_Q; ++q) {
+                    w[FIR_R + q] = row[FIR_R + q];
+                    const R c = tp[q * a.decim];
+#pragma unroll
+                    for (int r = 0; r < FIR_R; ++r) acc[r] = fma(c, w[q + r], acc[r]);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < FIR_R; ++r) {
+                if (k0 + r < a.bins) {
+                    const float v = (float)acc[r];
+                    eo[k0 + r] = v > 0.0f ? v : 0.0f;
+                }
+            }
+        }
+    } else {
+        // generic tap count: plain polyphase loops
+        for (int64_t k = tid; k < a.bins; k += kGroupThreads) {
+            R acc = 0;
+            for (int p = 0; p < a.decim; ++p) {
+                const R* row = ph + p * a.phase_len + k;
+                for (int q = 0; q < a.fir_q; ++q) acc = fma(comp[q * a.decim + p], row[q], acc);
+            }
+            const float v = (float)acc;
+            eo[k] = v > 0.0f ? v : 0.0f;
+        }
+    }
+}
+
+template <typename R, int G, int M>
+__global__ void __launch_bounds__(kThreads * G, 2 / G) k_envelope(EnvArgs a) {
     using V = typename Cx<R>::T;
     extern __shared__ __align__(16) unsigned char smem[];
-    const int N = a.n, M = N / 2;
-    R* bufA = reinterpret_cast<R*>(smem);                    // N real
-    V* bufB = reinterpret_cast<V*>(bufA + N);                // M + M/16 complex
-    R* comp = reinterpret_cast<R*>(bufB + M + M / 16);       // comp_len
-    int* sh = reinterpret_cast<int*>(comp + a.comp_len);     // 32 shifts
-    const R* filt = reinterpret_cast<const R*>(a.filt);
+    constexpr int N = 2 * M;
+    const int grp = gidx(), tid = gtid();
+    R* comp = reinterpret_cast<R*>(smem);
+    const int comp_pad = (a.fir_q * a.decim + 1) & ~1;
+    V* bufB = reinterpret_cast<V*>(comp + comp_pad) + (size_t)grp * (M + M / 16);
     const R* cr = reinterpret_cast<const R*>(a.comp);
     const V* tw = reinterpret_cast<const V*>(a.tw);
-    for (int i = threadIdx.x; i < a.comp_len; i += blockDim.x) comp[i] = cr[i];
+    for (int i = threadIdx.x; i < comp_pad; i += blockDim.x) comp[i] = i < a.comp_len ? cr[i] : (R)0;
+    __syncthreads();
     const int64_t L = a.mf_len;
     const int64_t items = a.n_dirs * a.batch;
     const R scale = (R)2 / (R)N;
     const int c0 = (a.comp_len - 1) / 2;
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int64_t b = it / a.n_dirs, d = it % a.n_dirs;
-        if (threadIdx.x < 32) sh[threadIdx.x] = a.shifts[d * 32 + threadIdx.x];
-        __syncthreads();
-        // delay-and-sum, channels accumulated in order 0..31 then * (1/32)
-        const R* fb = filt + (size_t)b * 32 * L;
-        for (int64_t n = threadIdx.x; n < N; n += blockDim.x) {
-            R acc = 0;
-            if (n < L) {
-#pragma unroll 8
-                for (int i = 0; i < 32; ++i) {
-                    const int64_t src = n - sh[i];
-                    if (src >= 0 && src < L) acc += fb[(size_t)i * L + src];
-                }
-                acc *= (R)(1.0 / 32.0);
-            }
-            bufA[n] = acc;
-        }
-        __syncthreads();
-        cfft<false, false>(reinterpret_cast<const V*>(bufA), bufB, M, tw, 2);
+    R* env = reinterpret_cast<R*>(bufB); // env[n] at n + 2*(n >> 5) (pad16 of the complex view)
+    for (int64_t it = (int64_t)blockIdx.x * G + grp; it < items; it += (int64_t)gridDim.x * G) {
+        const int64_t b = it / a.n_dirs, slot = it % a.n_dirs;
+        const R* src = reinterpret_cast<const R*>(a.beams) + (size_t)it * N;
+        cfft<M, false, false>(reinterpret_cast<const V*>(src), bufB, tw, 2);
         real_spectral_op(bufB, M, tw, [&](V X, int k) {
             if (k == 0 || k == M) return V{(R)0, (R)0};
             return V{X.y * scale, -X.x * scale}; // -i X, with the 2/N of the inverse
         });
-        cfft<true, true>(bufB, bufB, M, tw, 2);
-        for (int64_t n = threadIdx.x; n < L; n += blockDim.x) {
-            const V z = bufB[pad16((int)(n >> 1))];
-            const R h = (n & 1) ? z.y : z.x;
-            const R bv = bufA[n];
-            bufA[n] = sqrt(bv * bv + h * h);
-        }
-        __syncthreads();
-        float* eo = a.energy + (size_t)it * a.bins;
-        for (int64_t k = threadIdx.x; k < a.bins; k += blockDim.x) {
-            const int64_t s = k * a.decim - c0;
-            const int64_t lo = s > 0 ? s : 0, hi = ((s + a.comp_len) < L ? (s + a.comp_len) : L);
-            const R* hh = comp + (lo - s);
-            const R* xx = bufA + lo;
-            const int cnt = (int)(hi - lo);
-            R a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-            int j = 0;
-            for (; j + 4 <= cnt; j += 4) {
-                a0 += hh[j] * xx[j];
-                a1 += hh[j + 1] * xx[j + 1];
-                a2 += hh[j + 2] * xx[j + 2];
-                a3 += hh[j + 3] * xx[j + 3];
+        cfft<M, true, true>(bufB, bufB, tw, 2);
+        // |b + iH(b)|: h from the inverse FFT (shared), b re-read from the beam
+        // buffer; values kept in registers across the barrier, then written in
+        // the decimation-phase layout e_p[u] = env[u*D - c0 + p] (zero outside
+        // [0, L)) that the polyphase FIR below reads with unit stride.
+        constexpr int NV = (2 * M + kGroupThreads - 1) / kGroupThreads;
+        R ev[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int n = tid + i * kGroupThreads;
+            ev[i] = 0;
+            if (n < L) {
+                const R h = env[n + 2 * (n >> 5)];
+                const R bv = src[n];
+                ev[i] = sqrt(bv * bv + h * h);
             }
-            R acc = (a0 + a1) + (a2 + a3);
-            for (; j < cnt; ++j) acc += hh[j] * xx[j];
-            const float v = (float)acc;
-            eo[k] = v > 0.0f ? v : 0.0f;
         }
-        __syncthreads();
+        gsync();
+        R* ph = env; // phases: D rows of U entries
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int n = tid + i * kGroupThreads;
+            if (n < L) {
+                const int t = n + c0;
+                ph[(t % a.decim) * a.phase_len + t / a.decim] = ev[i];
+            }
+        }
+        // zero the phase slots whose sample lies outside [0, L)
+        for (int idx = tid; idx < a.decim * a.phase_len; idx += kGroupThreads) {
+            const int p = idx / a.phase_len, u = idx - p * a.phase_len;
+            const int64_t n = (int64_t)u * a.decim - c0 + p;
+            if (n < 0 || n >= L) ph[idx] = 0;
+        }
+        gsync();
+        float* eo = a.energy + ((size_t)b * a.n_dirs + a.order[slot]) * a.bins;
+        fir_polyphase<R>(ph, comp, a, eo);
+        gsync();
     }
 }
 
@@ -371,25 +488,91 @@ void launch_premf(const PremfArgs& a, int batch, cudaStream_t s) {
     k_premf<<<dim3(gx, 32, batch), kThreads, smem, s>>>(a);
 }
 
-void launch_matched_filter(const MfArgs& a, int batch, size_t smem, cudaStream_t s) {
-    set_smem((const void*)k_matched_filter, smem);
-    k_matched_filter<<<dim3(32, batch), kThreads, smem, s>>>(a);
+template <int M>
+static void mf_launch(const MfArgs& a, int batch, size_t smem, cudaStream_t s) {
+    set_smem((const void*)k_matched_filter<M>, smem);
+    k_matched_filter<M><<<dim3(32, batch), kThreads, smem, s>>>(a);
 }
 
-void launch_directions_f64(const DirArgs& a, int grid, size_t smem, cudaStream_t s) {
-    set_smem((const void*)k_directions<double>, smem);
-    k_directions<double><<<grid, kThreads, smem, s>>>(a);
+template <typename R>
+static void launch_bf(const BeamArgs& a, cudaStream_t s) {
+    const size_t smem = (size_t)32 * (a.T + 2 * a.H) * sizeof(R);
+    set_smem((const void*)k_beamform_tiles<R>, smem);
+    dim3 grid((unsigned)((a.L + a.T - 1) / a.T), (unsigned)((a.n_dirs + kThreads - 1) / kThreads),
+              (unsigned)a.batch);
+    k_beamform_tiles<R><<<grid, kThreads, smem, s>>>(a);
 }
 
-void launch_directions_f32(const DirArgs& a, int grid, size_t smem, cudaStream_t s) {
-    set_smem((const void*)k_directions<float>, smem);
-    k_directions<float><<<grid, kThreads, smem, s>>>(a);
+void launch_beamform_tiles(const BeamArgs& a, bool f32, cudaStream_t s) {
+    if (f32) launch_bf<float>(a, s);
+    else launch_bf<double>(a, s);
+}
+
+size_t envelope_smem_bytes(int n, int comp_taps_padded, bool f32, int groups) {
+    const size_t rb = f32 ? 4 : 8;
+    const int M = n / 2;
+    return (size_t)((comp_taps_padded + 1) & ~1) * rb + (size_t)groups * (M + M / 16) * 2 * rb;
+}
+
+// Compile-time FFT sizes: N = 2M real points, 32 <= N <= 8192.
+#define SNB_DISPATCH_M(M_RUNTIME, CALL)                                  \
+    switch (M_RUNTIME) {                                                 \
+        case 16: { constexpr int MM = 16; CALL; break; }                 \
+        case 32: { constexpr int MM = 32; CALL; break; }                 \
+        case 64: { constexpr int MM = 64; CALL; break; }                 \
+        case 128: { constexpr int MM = 128; CALL; break; }               \
+        case 256: { constexpr int MM = 256; CALL; break; }               \
+        case 512: { constexpr int MM = 512; CALL; break; }               \
+        case 1024: { constexpr int MM = 1024; CALL; break; }             \
+        case 2048: { constexpr int MM = 2048; CALL; break; }             \
+        case 4096: { constexpr int MM = 4096; CALL; break; }             \
+        default: break;                                                  \
+    }
+
+template <typename R, int G, int M>
+static int env_occ(size_t smem) {
+    int n = 1;
+    set_smem((const void*)k_envelope<R, G, M>, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_envelope<R, G, M>, kThreads * G, smem);
+    return n;
+}
+
+int envelope_blocks_per_sm(bool f32, int n_fft, size_t smem) {
+    int n = 1;
+    if (f32) { SNB_DISPATCH_M(n_fft / 2, (n = env_occ<float, kEnvGroupsF32, MM>(smem))) }
+    else { SNB_DISPATCH_M(n_fft / 2, (n = env_occ<double, kEnvGroupsF64, MM>(smem))) }
+    return n > 0 ? n : 1;
+}
+
+template <typename R, int G, int M>
+static void env_launch(const EnvArgs& a, int grid, size_t smem, cudaStream_t s) {
+    set_smem((const void*)k_envelope<R, G, M>, smem);
+    k_envelope<R, G, M><<<grid, kThreads * G, smem, s>>>(a);
+}
+
+void launch_envelope(const EnvArgs& a, bool f32, int grid, cudaStream_t s) {
+    if (f32) {
+        const size_t smem = envelope_smem_bytes(a.n, a.fir_q * a.decim, true, kEnvGroupsF32);
+        SNB_DISPATCH_M(a.n / 2, (env_launch<float, kEnvGroupsF32, MM>(a, grid, smem, s)))
+    } else {
+        const size_t smem = envelope_smem_bytes(a.n, a.fir_q * a.decim, false, kEnvGroupsF64);
+        SNB_DISPATCH_M(a.n / 2, (env_launch<double, kEnvGroupsF64, MM>(a, grid, smem, s)))
+    }
+}
+
+template <int M>
+static void rfft_launch(const double* x, double2* X, const double2* tw, size_t smem, cudaStream_t s) {
+    set_smem((const void*)k_rfft_forward<M>, smem);
+    k_rfft_forward<M><<<1, kThreads, smem, s>>>(x, X, tw);
 }
 
 void launch_rfft_forward(const double* x, double2* X, const double2* tw, int n, size_t smem,
                          cudaStream_t s) {
-    set_smem((const void*)k_rfft_forward, smem);
-    k_rfft_forward<<<1, kThreads, smem, s>>>(x, X, tw, n);
+    SNB_DISPATCH_M(n / 2, (rfft_launch<MM>(x, X, tw, smem, s)))
+}
+
+void launch_matched_filter(const MfArgs& a, int batch, size_t smem, cudaStream_t s) {
+    SNB_DISPATCH_M(a.n / 2, (mf_launch<MM>(a, batch, smem, s)))
 }
 
 } // namespace snb

@@ -7,12 +7,13 @@
 //   strided_filter pre-MF /2         (filters.hpp:14-39)      -> k_premf
 //   matched filter via RealFft       (pipeline.cpp:555-562)    -> k_matched_filter
 //   run_directions: beamform_into + envelope_direction
-//                                    (pipeline.cpp:432-505)    -> k_directions
+//                                    (pipeline.cpp:432-505)    -> k_beamform_tiles + k_envelope
 // Device layouts (batch index b outermost):
 //   packed  [b][frames*4 bytes]           u8   (as received)
 //   demod   [b][32][demod_len]            f64
 //   mf      [b][32][mf_len]               f64
-//   filt    [b][32][mf_len]               f64  (+ f32 copy in F32 mode)
+//   filt    [b][32][Lp]  zero halo H      f64  (+ f32 copy in F32 mode)
+//   beams   [b][n_dirs][N] slot order     f64/f32 (tail [L, N) zero)
 //   energy  [b][n_dirs][bins]             f32
 #pragma once
 
@@ -48,25 +49,40 @@ struct MfArgs {
     float* filt32;          // optional f32 copy (F32 mode) or null
     const double2* ref_spec;// M+1 bins of rfft(reversed chirp, N)
     const double2* tw;      // e^{-2 pi i k/N}, k < N
-    int64_t mf_len;
-    int n, ref_len;
+    int64_t mf_len, Lp;
+    int n, ref_len, H;
 };
 
-struct DirArgs {
-    const void* filt;        // [B][32][mf_len] f64 or f32
-    float* energy;           // [B][n_dirs][bins]
-    const int32_t* shifts;   // [n_dirs][32] = delay - advance
+struct BeamArgs {
+    const void* filt;        // [B][32][Lp] f64/f32, sample n at H + n, zero halo
+    void* beams;             // [B][n_dirs][N] slot order, tail [L, N) zero
+    const int32_t* shifts;   // [n_dirs][32] slot order: delay - advance
+    int64_t L, Lp, N, n_dirs;
+    int H, T, batch;
+};
+
+struct EnvArgs {
+    const void* beams;       // [B][n_dirs][N] slot order
+    float* energy;           // [B][n_dirs][bins] direction order
+    const int32_t* order;    // slot -> direction
     const void* comp;        // composite reversed kernel (f64 or f32)
     const void* tw;          // twiddles for N (double2 or float2)
     int64_t mf_len, bins, n_dirs;
     int n, comp_len, decim, batch;
+    int fir_q;               // ceil(comp_len / decim): taps per phase
+    int phase_len;           // entries per phase row (>= bins + fir_q + FIR_R)
 };
+
+constexpr int kEnvGroupsF64 = 1;
+constexpr int kEnvGroupsF32 = 1;
 
 void launch_demod(const DemodArgs& a, int grid_x, size_t smem, cudaStream_t s);
 void launch_premf(const PremfArgs& a, int batch, cudaStream_t s);
 void launch_matched_filter(const MfArgs& a, int batch, size_t smem, cudaStream_t s);
-void launch_directions_f64(const DirArgs& a, int grid, size_t smem, cudaStream_t s);
-void launch_directions_f32(const DirArgs& a, int grid, size_t smem, cudaStream_t s);
+void launch_beamform_tiles(const BeamArgs& a, bool f32, cudaStream_t s);
+void launch_envelope(const EnvArgs& a, bool f32, int grid, cudaStream_t s);
+size_t envelope_smem_bytes(int n, int comp_taps_padded, bool f32, int groups);
+int envelope_blocks_per_sm(bool f32, int n_fft, size_t smem);
 void launch_rfft_forward(const double* x, double2* X, const double2* tw, int n, size_t smem,
                          cudaStream_t s);
 

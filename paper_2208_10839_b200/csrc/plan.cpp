@@ -391,6 +391,41 @@ Plan make_plan(const sn_pipeline_config& cin) {
         }
         p.advances[d] = static_cast<int32_t>(std::llround(-lo * s.mf_rate));
     }
+    // Direction schedule: sort directions along a Morton curve over the
+    // boresight-plane components (u_y, u_z) of their unit vectors so that the
+    // 32 directions a warp beamforms together have nearby per-channel shifts
+    // (a shared-memory load then serves all 32 lanes from one or two
+    // 128-byte wavefronts).
+    {
+        std::vector<std::pair<uint64_t, int32_t>> keyed(s.n_dirs);
+        for (uint64_t d = 0; d < s.n_dirs; ++d) {
+            const V3 u = unit_vector(p.directions[2 * d], p.directions[2 * d + 1]);
+            auto q = [](double v) {
+                const double t = std::clamp((v + 1.0) * 0.5, 0.0, 1.0);
+                return static_cast<uint32_t>(t * 65535.0 + 0.5);
+            };
+            const uint32_t a = q(u.y), b = q(u.z);
+            uint64_t key = 0;
+            for (int bit = 15; bit >= 0; --bit) {
+                key = (key << 2) | (((b >> bit) & 1u) << 1) | ((a >> bit) & 1u);
+            }
+            keyed[d] = {key, static_cast<int32_t>(d)};
+        }
+        std::stable_sort(keyed.begin(), keyed.end());
+        p.order.resize(s.n_dirs);
+        p.shifts.resize(s.n_dirs * kCh);
+        int32_t halo = 0;
+        for (uint64_t slot = 0; slot < s.n_dirs; ++slot) {
+            const int32_t d = keyed[slot].second;
+            p.order[slot] = d;
+            for (int i = 0; i < kCh; ++i) {
+                const int32_t sh = p.delays[d * kCh + i] - p.advances[d];
+                p.shifts[slot * kCh + i] = sh;
+                halo = std::max(halo, std::abs(sh));
+            }
+        }
+        p.halo = halo;
+    }
     // Composite smoothing (127 taps) * post-envelope anti-alias (321 taps)
     // (pipeline.cpp:307-318).
     const auto smooth = design_lowpass(c.smoothing_cutoff_hz, s.mf_rate, c.smoothing_taps);

@@ -48,6 +48,11 @@ struct Plan {
     std::vector<double> comp_rev;     // reversed composite smoothing+anti-alias kernel
     std::vector<int32_t> delays;      // n_dirs x 32 at the MF rate
     std::vector<int32_t> advances;    // n_dirs
+    // Device scheduling of the direction loop (no effect on results: every
+    // direction is independent, pipeline.cpp:225-226):
+    std::vector<int32_t> order;       // slot -> direction, Morton order of (u_y, u_z)
+    std::vector<int32_t> shifts;      // slot-major [n_dirs][32]: delay - advance
+    int32_t halo = 0;                 // max |shift| over all directions/channels
 };
 
 // Validates (pipeline.cpp:60-92; geometry.cpp:27-57 invariants; Direction

@@ -97,6 +97,9 @@ struct sn_workspace {
     double* d_mf = nullptr;
     double* d_filt = nullptr;
     float* d_filt32 = nullptr;
+    void* d_beams = nullptr;
+    int32_t* d_order = nullptr;
+    int32_t* d_shifts_slot = nullptr;
     float* d_energy = nullptr;
     double* d_lut = nullptr;
     double* d_premf = nullptr;
@@ -113,12 +116,12 @@ struct sn_workspace {
     DemodArgs demod{};
     int demod_grid = 0;
     size_t demod_smem = 0, mf_smem = 0, dir_smem = 0;
-    int dir_grid = 0;
-    uint64_t packed_bytes = 0, energy_per = 0;
+    int dir_grid = 0, halo = 0, tile = 0, fir_q = 0, phase_len = 0;
+    uint64_t packed_bytes = 0, energy_per = 0, lp = 0;
     uint64_t alloc_events = 0, device_allocs = 0, last_launches = 0;
     // optional per-stage timing (events on the launching stream)
     bool profiling = false;
-    cudaEvent_t ev[5] = {};
+    cudaEvent_t ev[6] = {};
     // graph cache
     cudaGraphExec_t graph = nullptr;
     const uint8_t* g_in = nullptr;
@@ -135,7 +138,7 @@ struct sn_workspace {
             if (e) cudaEventDestroy(e);
         }
         for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
-                        (void*)d_filt32, (void*)d_energy, (void*)d_lut, (void*)d_premf,
+                        (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot, (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
                         (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32}) {
             if (p) cudaFree(p);
@@ -166,8 +169,21 @@ struct sn_workspace {
         d_packed = dmalloc<uint8_t>(B * packed_bytes, n);
         d_demod = dmalloc<double>(B * kCh * s.demod_len, n);
         d_mf = dmalloc<double>(B * kCh * s.mf_len, n);
-        d_filt = dmalloc<double>(B * kCh * s.mf_len, n);
-        if (f32) d_filt32 = dmalloc<float>(B * kCh * s.mf_len, n);
+        halo = plan.halo;
+        lp = s.mf_len + 2 * static_cast<uint64_t>(halo);
+        d_filt = dmalloc<double>(B * kCh * lp, n);
+        ck(cudaMemsetAsync(d_filt, 0, B * kCh * lp * sizeof(double), stream), "memset");
+        if (f32) {
+            d_filt32 = dmalloc<float>(B * kCh * lp, n);
+            ck(cudaMemsetAsync(d_filt32, 0, B * kCh * lp * sizeof(float), stream), "memset");
+        }
+        const size_t beam_bytes = B * s.n_dirs * s.env_fft * (f32 ? sizeof(float) : sizeof(double));
+        d_beams = dmalloc<uint8_t>(beam_bytes, n);
+        ck(cudaMemsetAsync(d_beams, 0, beam_bytes, stream), "memset");
+        d_order = dmalloc<int32_t>(s.n_dirs, n);
+        d_shifts_slot = dmalloc<int32_t>(s.n_dirs * kCh, n);
+        upload(d_order, plan.order, stream);
+        upload(d_shifts_slot, plan.shifts, stream);
         d_energy = dmalloc<float>(B * energy_per, n);
         d_lut = dmalloc<double>(plan.demod_lut.size(), n);
         d_premf = dmalloc<double>(plan.premf_rev.size(), n);
@@ -239,10 +255,29 @@ struct sn_workspace {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const int per_sm = std::max(1, (int)((228 * 1024) / (demod_smem + 1024)));
         demod_grid = std::max(1, sms * per_sm / P);
-        dir_smem = fft_smem_bytes((int)s.env_fft, f32 ? sizeof(float) : sizeof(double)) +
-                   plan.comp_rev.size() * (f32 ? sizeof(float) : sizeof(double)) + 32 * sizeof(int);
-        const int dir_per_sm = std::max(1, (int)((228 * 1024) / (dir_smem + 1024)));
-        dir_grid = sms * dir_per_sm;
+        // beamformer time tile: 32 x (T + 2H) samples staged per CTA
+        tile = 128;
+        {
+            const int D = plan.cfg.post_envelope_decimation;
+            fir_q = (int)((plan.comp_rev.size() + D - 1) / D);
+            phase_len = (int)s.bins + fir_q + 16;
+            // the phase rows live in the FFT buffer: D * phase_len <= 2 * (M + M/16)
+            const uint64_t M = s.env_fft / 2;
+            if ((uint64_t)D * phase_len > 2 * (M + M / 16)) {
+                config_error("pipeline: post-envelope FIR does not fit the device envelope buffer");
+            }
+            if (s.mf_len + (plan.comp_rev.size() - 1) / 2 >= (uint64_t)D * phase_len) {
+                phase_len = (int)((s.mf_len + plan.comp_rev.size()) / D + 2);
+                if ((uint64_t)D * phase_len > 2 * (M + M / 16)) {
+                    config_error("pipeline: post-envelope FIR does not fit the device envelope buffer");
+                }
+            }
+        }
+        dir_smem = envelope_smem_bytes((int)s.env_fft, fir_q * plan.cfg.post_envelope_decimation, f32,
+                                       f32 ? kEnvGroupsF32 : kEnvGroupsF64);
+        {
+            dir_grid = sms * envelope_blocks_per_sm(f32, (int)s.env_fft, dir_smem);
+        }
         mf_smem = fft_smem_bytes((int)s.mf_fft, sizeof(double));
         ck(cudaStreamSynchronize(stream), "setup sync");
     }
@@ -262,28 +297,41 @@ struct sn_workspace {
         launch_premf(pa, (int)count, s);
         if (profiling) cudaEventRecord(ev[2], s);
         MfArgs ma{d_mf, d_filt, f32 ? d_filt32 : nullptr, d_ref_spec, d_tw_mf,
-                  (int64_t)z.mf_len, (int)z.mf_fft, (int)z.ref_len};
+                  (int64_t)z.mf_len, (int64_t)lp, (int)z.mf_fft, (int)z.ref_len, halo};
         launch_matched_filter(ma, (int)count, mf_smem, s);
         if (profiling) cudaEventRecord(ev[3], s);
-        DirArgs ra{};
-        ra.filt = f32 ? (const void*)d_filt32 : (const void*)d_filt;
-        ra.energy = d_out;
-        ra.shifts = d_shifts;
-        ra.comp = f32 ? (const void*)d_comp32 : (const void*)d_comp;
-        ra.tw = f32 ? (const void*)d_tw_env32 : (const void*)d_tw_env;
-        ra.mf_len = (int64_t)z.mf_len;
-        ra.bins = (int64_t)z.bins;
-        ra.n_dirs = (int64_t)z.n_dirs;
-        ra.n = (int)z.env_fft;
-        ra.comp_len = (int)plan.comp_rev.size();
-        ra.decim = plan.cfg.post_envelope_decimation;
-        ra.batch = (int)count;
-        const int grid = (int)std::min<int64_t>(dir_grid, (int64_t)(z.n_dirs * count));
-        if (f32) launch_directions_f32(ra, grid, dir_smem, s);
-        else launch_directions_f64(ra, grid, dir_smem, s);
+        BeamArgs ba{};
+        ba.filt = f32 ? (const void*)d_filt32 : (const void*)d_filt;
+        ba.beams = d_beams;
+        ba.shifts = d_shifts_slot;
+        ba.L = (int64_t)z.mf_len;
+        ba.Lp = (int64_t)lp;
+        ba.N = (int64_t)z.env_fft;
+        ba.n_dirs = (int64_t)z.n_dirs;
+        ba.H = halo;
+        ba.T = tile;
+        ba.batch = (int)count;
+        launch_beamform_tiles(ba, f32, s);
         if (profiling) cudaEventRecord(ev[4], s);
+        EnvArgs ea{};
+        ea.beams = d_beams;
+        ea.energy = d_out;
+        ea.order = d_order;
+        ea.comp = f32 ? (const void*)d_comp32 : (const void*)d_comp;
+        ea.tw = f32 ? (const void*)d_tw_env32 : (const void*)d_tw_env;
+        ea.mf_len = (int64_t)z.mf_len;
+        ea.bins = (int64_t)z.bins;
+        ea.n_dirs = (int64_t)z.n_dirs;
+        ea.n = (int)z.env_fft;
+        ea.comp_len = (int)plan.comp_rev.size();
+        ea.decim = plan.cfg.post_envelope_decimation;
+        ea.batch = (int)count;
+        ea.fir_q = fir_q;
+        ea.phase_len = phase_len;
+        launch_envelope(ea, f32, dir_grid, s);
+        if (profiling) cudaEventRecord(ev[5], s);
         ck(cudaGetLastError(), "kernel launch");
-        last_launches = 4;
+        last_launches = 5;
     }
 
     void validate(const sn_raw_measurement& m) const { // pipeline.cpp:524-540
@@ -510,7 +558,7 @@ sn_status sn_workspace_process_device_graph(sn_workspace* ws, const uint8_t* d_p
             ws->g_count = count;
         }
         ck(cudaGraphLaunch(ws->graph, s), "graph launch");
-        ws->last_launches = 4;
+        ws->last_launches = 5;
     });
 }
 
@@ -565,13 +613,18 @@ sn_status sn_workspace_stage(sn_workspace* ws, int32_t stage, uint64_t item, dou
         switch (stage) {
             case SN_STAGE_DEMOD: src = ws->d_demod + item * kCh * z.demod_len; n = kCh * z.demod_len; break;
             case SN_STAGE_PREMF: src = ws->d_mf + item * kCh * z.mf_len; n = kCh * z.mf_len; break;
-            case SN_STAGE_FILT: src = ws->d_filt + item * kCh * z.mf_len; n = kCh * z.mf_len; break;
+            case SN_STAGE_FILT: src = ws->d_filt + item * kCh * ws->lp + ws->halo; n = kCh * z.mf_len; break;
             default: argument_error("unknown stage");
         }
         if (capacity < n) argument_error("buffer too small");
         DeviceGuard g(ws->device);
         ck(cudaStreamSynchronize(ws->stream), "sync");
-        ck(cudaMemcpy(out, src, n * sizeof(double), cudaMemcpyDeviceToHost), "stage copy");
+        if (stage == SN_STAGE_FILT) {
+            ck(cudaMemcpy2D(out, z.mf_len * sizeof(double), src, ws->lp * sizeof(double),
+                            z.mf_len * sizeof(double), kCh, cudaMemcpyDeviceToHost), "stage copy");
+        } else {
+            ck(cudaMemcpy(out, src, n * sizeof(double), cudaMemcpyDeviceToHost), "stage copy");
+        }
     });
 }
 
@@ -614,14 +667,14 @@ sn_status sn_workspace_set_profiling(sn_workspace* ws, int enable) {
     });
 }
 
-sn_status sn_workspace_stage_times(sn_workspace* ws, float* ms4) {
+sn_status sn_workspace_stage_times(sn_workspace* ws, float* ms5) {
     return guarded([&] {
-        if (!ws || !ms4) argument_error("null argument");
+        if (!ws || !ms5) argument_error("null argument");
         ws->require_device();
         if (!ws->profiling) argument_error("profiling is not enabled");
         DeviceGuard g(ws->device);
-        ck(cudaEventSynchronize(ws->ev[4]), "event sync");
-        for (int i = 0; i < 4; ++i) ck(cudaEventElapsedTime(&ms4[i], ws->ev[i], ws->ev[i + 1]), "elapsed");
+        ck(cudaEventSynchronize(ws->ev[5]), "event sync");
+        for (int i = 0; i < 5; ++i) ck(cudaEventElapsedTime(&ms5[i], ws->ev[i], ws->ev[i + 1]), "elapsed");
     });
 }
 
