@@ -266,7 +266,7 @@ class RefWorkspace:
     def bit_rows(self):
         stride = self.dims["frames"] // 8 + self.dims["lut_octets"]
         out = np.zeros(32 * stride, np.uint8)
-        self.ref._check(self.ref.lib.ref_ws_stage(self.h, 3, out.ctypes.data, out.size // 8))
+        self.ref._check(self.ref.lib.ref_ws_stage(self.h, 3, out.ctypes.data, out.size))
         return out.reshape(32, stride)
 
     def table(self, which: int):

@@ -369,8 +369,8 @@ struct sn_workspace {
     // page-locked are DMA'd directly; pageable ones go through the
     // workspace's pinned staging buffers.
     void process_host(const sn_raw_measurement* ms, uint64_t count, float* out) {
-        require_device();
         for (uint64_t i = 0; i < count; ++i) validate(ms[i]); // all-or-error
+        require_device();
         DeviceGuard g(device);
         const bool out_pinned = is_pinned(out);
         uint64_t done = 0;

@@ -1,0 +1,347 @@
+"""GPU parity tests (run on the B200): the CUDA path through the C ABI against
+the unmodified reference (oracle/_ref), the C restatement and the golden
+fixtures, plus the reference's own behavioural oracles
+(test_pipeline.cpp:268-519).
+
+Tolerances (stated):
+  * demodulation (demod_buf) and pre-MF decimation (mf_buf): bit-exact.
+  * matched filter (filt_buf), FP64: relative RMS <= 1e-13 (FFT route vs the
+    reference's FFTW route; both ~1e-16 from exact).
+  * energyscape, FP64 mode: relative RMS <= 1e-12 and max |diff| <= 1e-9 x
+    peak; on the golden fixtures the float32 output is required to be
+    bit-identical to the reference.
+  * energyscape, FP32 mode: relative RMS <= 1e-6 (the reference's own
+    cross-route bound, test_pipeline.cpp:494) and max |diff| <= 1e-5 x peak.
+"""
+import numpy as np
+import pytest
+
+from conftest import TINY, TINY_SCENE, az181, golden, rel_rms, to_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu(sn):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return sn
+
+
+def cfg_for(sn, name, precision=0):
+    base = sn.default_pipeline_config(sn.GridKind.horizontal90)
+    cfgs = {
+        "tiny": lambda: base.copy(**TINY),
+        "small": lambda: base.copy(max_range=1.5),
+        "h90": lambda: base,
+        "az181": lambda: base.copy(directions=az181(), grid_kind=3),
+        "box1850": lambda: sn.default_pipeline_config(sn.GridKind.box1850),
+        "hemi3000": lambda: sn.default_pipeline_config(sn.GridKind.hemisphere3000),
+        "small_box": lambda: sn.default_pipeline_config(sn.GridKind.box1850).copy(max_range=1.5),
+    }
+    return cfgs[name]().copy(precision=precision)
+
+
+def capture(sn, cfg, reflectors, noise=0.01, seed=7, serial=1, ts=0, seq=0):
+    return sn.synthesize_measurement(cfg, sn.Scene([sn.Reflector(*r) for r in reflectors], noise, seed),
+                                     serial, ts, seq)
+
+
+def check_f64(got, want):
+    assert got.shape == want.shape
+    assert rel_rms(got, want) <= 1e-12
+    assert np.abs(got.astype(np.float64) - want).max() <= 1e-9 * max(float(want.max()), 1e-30)
+
+
+def check_f32(got, want):
+    assert got.shape == want.shape
+    assert rel_rms(got, want) <= 1e-6
+    assert np.abs(got.astype(np.float64) - want).max() <= 1e-5 * float(want.max())
+
+
+# ---------------------------------------------------------------------------
+def test_golden_tiny_bit_exact_all_stages(gpu):
+    sn = gpu
+    g = golden("tiny.npz")
+    cfg = cfg_for(sn, "tiny")
+    ws = sn.Workspace(cfg, device=0)
+    m = sn.RawMeasurement(1, 1000, 0, 32, ws.frames, cfg.pdm_rate, g["packed"])
+    img = ws.process(m)
+    assert np.array_equal(ws.stage(0), g["demod"])
+    assert np.array_equal(ws.stage(1), g["mf"])
+    assert rel_rms(ws.stage(2), g["filt"]) <= 1e-13
+    assert np.array_equal(img.energies, g["energies"])
+    assert img.sensor_serial == 1 and img.timestamp_us == 1000 and img.range_bins == 58
+
+
+def test_golden_h90_bit_exact(gpu, po):
+    sn = gpu
+    h = golden("h90.npz")
+    cfg = cfg_for(sn, "h90")
+    m = capture(sn, cfg, po.BENCH_SCENE, po.BENCH_NOISE, po.BENCH_SEED)
+    img = sn.Workspace(cfg, device=0).process(m)
+    assert np.array_equal(img.energies, h["energies"])
+
+
+@pytest.mark.parametrize("name", ["small", "h90", "az181", "box1850", "hemi3000", "small_box"])
+def test_parity_vs_reference_f64(gpu, po, ref, name):
+    sn = gpu
+    cfg = cfg_for(sn, name)
+    rng = np.random.default_rng(hash(name) % 2**32)
+    rmax = 0.6 * cfg.max_range
+    refl = [(rng.uniform(0.3, rmax), rng.uniform(-0.7, 0.7), rng.uniform(-0.3, 0.3) if name not in ("h90", "az181", "small") else 0.0,
+             rng.uniform(0.3, 1.0)) for _ in range(2)]
+    m = capture(sn, cfg, refl, 0.01, 11)
+    ws = sn.Workspace(cfg, device=0)
+    img = ws.process(m)
+    rws = ref.workspace(to_oracle(po, cfg))
+    want = rws.process(m.packed)
+    assert np.array_equal(ws.stage(0), rws.stage(0))
+    assert np.array_equal(ws.stage(1), rws.stage(1))
+    assert rel_rms(ws.stage(2), rws.stage(2)) <= 1e-13
+    check_f64(img.energies, want)
+    assert img.argmax() == tuple(int(x) for x in np.unravel_index(np.argmax(want), want.shape))
+
+
+@pytest.mark.parametrize("name", ["tiny", "h90", "hemi3000"])
+def test_parity_vs_reference_f32(gpu, po, ref, name):
+    sn = gpu
+    cfg = cfg_for(sn, name, precision=1)
+    m = capture(sn, cfg, [(0.8 if name == "tiny" else 1.5, 0.2, 0.0, 0.8)], 0.01, 5)
+    img = sn.Workspace(cfg, device=0).process(m)
+    want = ref.workspace(to_oracle(po, cfg)).process(m.packed)
+    check_f32(img.energies, want)
+    assert img.argmax() == tuple(int(x) for x in np.unravel_index(np.argmax(want), want.shape))
+
+
+@pytest.mark.parametrize("byte", [0x00, 0xFF, 0xAA, 0x0F, 0x81])
+def test_known_answer_bit_patterns(gpu, po, ref, byte):
+    # constant / periodic bitstreams (test_dsp.cpp:85-101 spirit): every
+    # stage against the reference, demod bit-exact
+    sn = gpu
+    cfg = cfg_for(sn, "tiny")
+    ws = sn.Workspace(cfg, device=0)
+    pk = np.full(32 * ws.frames // 8, byte, np.uint8)
+    img = ws.process(sn.RawMeasurement(1, 0, 0, 32, ws.frames, cfg.pdm_rate, pk))
+    rws = ref.workspace(to_oracle(po, cfg))
+    want = rws.process(pk)
+    assert np.array_equal(ws.stage(0), rws.stage(0))
+    assert np.array_equal(ws.stage(1), rws.stage(1))
+    check_f64(img.energies, want)
+    if byte in (0x00, 0xFF):  # DC gain 1: the demodulated +-1 stays +-1 (test_dsp.cpp:240-254)
+        d = ws.stage(0)
+        sign = 1.0 if byte == 0xFF else -1.0
+        assert np.allclose(d[:, 20:-20], sign, atol=1e-3)
+
+
+def test_random_bitstream_vs_reference(gpu, po, ref):
+    sn = gpu
+    cfg = cfg_for(sn, "small")
+    ws = sn.Workspace(cfg, device=0)
+    pk = np.random.default_rng(3).integers(0, 256, 32 * ws.frames // 8, dtype=np.uint8)
+    img = ws.process(sn.RawMeasurement(1, 0, 0, 32, ws.frames, cfg.pdm_rate, pk))
+    rws = ref.workspace(to_oracle(po, cfg))
+    want = rws.process(pk)
+    assert np.array_equal(ws.stage(0), rws.stage(0))
+    check_f64(img.energies, want)
+
+
+def test_port_oracle_agrees(gpu, po, port):
+    sn = gpu
+    cfg = cfg_for(sn, "small_box")
+    m = capture(sn, cfg, [(0.9, 0.3, -0.2, 0.7)], 0.01, 9)
+    img = sn.Workspace(cfg, device=0).process(m)
+    want = port.process(to_oracle(po, cfg), m.packed)
+    check_f64(img.energies, want)
+
+
+# ---------------------------------------------------------------------------
+def test_batch_results_independent_of_batch(gpu):
+    sn = gpu
+    cfg = cfg_for(sn, "small")
+    ms = [capture(sn, cfg, [(0.4 + 0.1 * i, -0.5 + 0.2 * i, 0.0, 0.6)], 0.01, 20 + i, seq=i)
+          for i in range(6)]
+    single = sn.Workspace(cfg, device=0, max_batch=1)
+    batched = sn.Workspace(cfg, device=0, max_batch=4)  # 6 -> chunks of 4 + 2
+    a = [single.process(m).energies for m in ms]
+    b = [im.energies for im in batched.process_batch(ms)]
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_deterministic_and_workspace_transparent(gpu):
+    # test_pipeline.cpp:417-432 (thread-count independence) and
+    # test_nodes.cpp:396-445 (K=1 vs K=8 workers): identical bytes
+    sn = gpu
+    cfg = cfg_for(sn, "small")
+    m = capture(sn, cfg, [(1.0, 0.2, 0.0, 0.5)], 0.01, 77)
+    w1, w2 = sn.Workspace(cfg, device=0), sn.Workspace(cfg.copy(processing_threads=4), device=0)
+    r = [w1.process(m).energies, w1.process(m).energies, w2.process(m).energies]
+    assert np.array_equal(r[0], r[1]) and np.array_equal(r[0], r[2])
+
+
+def test_no_allocation_over_100_calls(gpu):
+    # test_pipeline.cpp:143-155
+    sn = gpu
+    cfg = cfg_for(sn, "small").copy(max_range=0.8, chirp_duration=1e-3)
+    ws = sn.Workspace(cfg, device=0)
+    m = capture(sn, cfg, [(0.5, 0.0, 0.0, 0.2)], 0.0, 0)
+    for _ in range(100):
+        ws.process(m)
+    assert ws.allocation_events() == 0
+
+
+def test_device_path_and_graph_replay_match_host_path(gpu):
+    import torch
+    sn = gpu
+    cfg = cfg_for(sn, "h90")
+    B = 3
+    ws = sn.Workspace(cfg, device=0, max_batch=B)
+    ms = [capture(sn, cfg, [(1.0 + 0.5 * i, 0.1 * i, 0.0, 0.7)], 0.01, 40 + i) for i in range(B)]
+    host = np.stack([im.energies for im in ws.process_batch(ms)])
+    dp = torch.from_numpy(np.stack([m.packed for m in ms])).cuda()
+    out = torch.empty((B, ws.n_dirs, ws.bins), dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    ws.process_device(dp.data_ptr(), B, out.data_ptr(), s.cuda_stream)
+    s.synchronize()
+    assert np.array_equal(out.cpu().numpy(), host)
+    out.zero_()
+    for _ in range(2):
+        ws.process_device(dp.data_ptr(), B, out.data_ptr(), s.cuda_stream, graph=True)
+    s.synchronize()
+    assert np.array_equal(out.cpu().numpy(), host)
+    assert ws.last_launches() == 5
+
+
+def test_decode_errors_on_device_workspace(gpu):
+    # test_pipeline.cpp:498-519: all-or-error
+    sn = gpu
+    cfg = cfg_for(sn, "small")
+    ws = sn.Workspace(cfg, device=0, max_batch=2)
+    m = capture(sn, cfg, [])
+    for bad in (dict(channels=16), dict(frames=m.frames - 8), dict(pdm_rate=1e6),
+                dict(packed=m.packed[:-1])):
+        with pytest.raises(sn.DecodeError):
+            ws.process(sn.RawMeasurement(**{**m.__dict__, **bad}))
+    with pytest.raises(sn.DecodeError):  # one bad capture fails the whole batch
+        ws.process_batch([m, sn.RawMeasurement(**{**m.__dict__, "channels": 8})])
+
+
+def test_beamform_accessor_bit_exact(gpu, po, ref):
+    # Workspace::beamform (pipeline.cpp:576-591) and its argument checks
+    sn = gpu
+    cfg = cfg_for(sn, "small")
+    ws = sn.Workspace(cfg, device=0)
+    L = ws.dims["mf_samples"]
+    x = np.random.default_rng(5).uniform(-1, 1, (32, L))
+    got = ws.beamform(x)
+    want = ref.workspace(to_oracle(po, cfg)).beamform(x)
+    assert np.array_equal(got, want)
+    assert np.array_equal(ws.beamform(2.5 * x), 2.5 * got)  # linearity (test_pipeline.cpp:247-262)
+    with pytest.raises(sn.ArgumentError):
+        ws.beamform(np.zeros((8, L)))
+    with pytest.raises(sn.ArgumentError):
+        ws.beamform(np.zeros((32, 100)))
+
+
+# ---- behavioural oracles (test_pipeline.cpp:268-415) --------------------------
+def nearest_direction(dirs, az, el):
+    return int(np.argmin(np.abs(dirs[:, 0] - az) + np.abs(dirs[:, 1] - el)))
+
+
+def expected_bin(cfg, rng_m):
+    return int(round(2.0 * rng_m / cfg.speed_of_sound * cfg.final_rate()))
+
+
+def one_reflector(sn, cfg, rng_m, az, el, amp, seed, noise=0.01):
+    return capture(sn, cfg, [(rng_m, az, el, amp * rng_m * rng_m)], noise, seed, ts=1000)
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_localization_within_one_cell(gpu, kind):
+    sn = gpu
+    cfg = sn.default_pipeline_config(kind).copy(max_range=1.5)
+    ws = sn.Workspace(cfg, device=0)
+    rng = np.random.default_rng(17)
+    hits = 0
+    for trial in range(12):
+        r = rng.uniform(0.6, 1.3)
+        max_az = 1.4 if kind == 0 else 0.7
+        az = rng.uniform(-max_az, max_az)
+        el = 0.0 if kind == 0 else rng.uniform(-0.7, 0.7)
+        img = ws.process(one_reflector(sn, cfg, r, az, el, rng.uniform(0.4, 0.8), trial * 31 + 5))
+        d, b = img.argmax()
+        want = nearest_direction(cfg.directions, az, el)
+        got_dir, want_dir = cfg.directions[d], cfg.directions[want]
+        ok = (abs(got_dir[0] - want_dir[0]) <= np.pi / 2 / 49 + 1e-9 and
+              abs(got_dir[1] - want_dir[1]) <= np.pi / 2 / 36 + 1e-9 and
+              abs(b - expected_bin(cfg, r)) <= 1)
+        hits += ok
+    assert hits >= 11  # acceptance.cpp:170-221 asks >= 96%
+
+
+def test_silence_floor(gpu):
+    sn = gpu
+    cfg = cfg_for(sn, "small")
+    ws = sn.Workspace(cfg, device=0)
+    silent = ws.process(capture(sn, cfg, [], 0.0, 0)).energies.max()
+    echo = ws.process(one_reflector(sn, cfg, 1.0, 0.0, 0.0, 1.0, 0, 0.0)).energies.max()
+    assert echo > 0 and silent <= 1e-6 * echo
+
+
+def test_two_reflectors_two_peaks(gpu):
+    sn = gpu
+    cfg = cfg_for(sn, "h90")
+    img = sn.Workspace(cfg, device=0).process(capture(
+        sn, cfg, [(1.0, -np.pi / 6, 0.0, 0.7), (2.0, 40 * np.pi / 180, 0.0, 0.7 * 4)], 0.01, 21))
+    e = img.energies
+    for az, r in ((-np.pi / 6, 1.0), (40 * np.pi / 180, 2.0)):
+        wd, wb = nearest_direction(cfg.directions, az, 0.0), expected_bin(cfg, r)
+        win = e[max(0, wd - 4):wd + 5, max(0, wb - 4):wb + 5]
+        d, b = np.unravel_index(np.argmax(win), win.shape)
+        assert abs(d + max(0, wd - 4) - wd) <= 1 and abs(b + max(0, wb - 4) - wb) <= 1
+
+
+def test_range_calibration_and_monotone_energy(gpu):
+    sn = gpu
+    cfg = cfg_for(sn, "h90")
+    ws = sn.Workspace(cfg, device=0)
+    prev = 1e30
+    for r in (0.5, 1.0, 2.0, 4.0):
+        img = ws.process(one_reflector(sn, cfg, r, 0.0, 0.0, 0.5, 33, 0.005))
+        assert abs(img.argmax()[1] - expected_bin(cfg, r)) <= 1
+        peak = ws.process(capture(sn, cfg, [(r, 0.0, 0.0, 0.5)], 0.0, 0)).energies.max()
+        assert peak < prev
+        prev = peak
+
+
+def test_amplitude_scaling_and_azimuth_monotonicity(gpu):
+    sn = gpu
+    cfg = cfg_for(sn, "small")
+    ws = sn.Workspace(cfg, device=0)
+    weak = ws.process(one_reflector(sn, cfg, 1.0, 0.3, 0.0, 0.3, 3, 0.0))
+    strong = ws.process(one_reflector(sn, cfg, 1.0, 0.3, 0.0, 0.6, 3, 0.0))
+    assert weak.argmax() == strong.argmax()
+    assert strong.energies.max() / weak.energies.max() == pytest.approx(2.0, rel=0.1)
+    prev = -1
+    for k in range(40, 45):
+        d, _ = ws.process(one_reflector(sn, cfg, 1.0, cfg.directions[k, 0], 0.0, 0.6, 55, 0.005)).argmax()
+        assert d > prev
+        prev = d
+
+
+def test_full_size_batch_properties(gpu):
+    # hemisphere3000, 16 captures: finite, clamped >= 0, each batch item equal
+    # to its own single-capture result (batch transparency at full size)
+    sn = gpu
+    cfg = cfg_for(sn, "hemi3000")
+    ms = [capture(sn, cfg, [(1.0 + 0.2 * i, 0.5 - 0.06 * i, 0.1, 0.6)], 0.01, 100 + i, seq=i)
+          for i in range(16)]
+    ws = sn.Workspace(cfg, device=0, max_batch=16)
+    imgs = ws.process_batch(ms)
+    e = np.stack([im.energies for im in imgs])
+    assert np.isfinite(e).all() and (e >= 0).all()
+    one = sn.Workspace(cfg, device=0, max_batch=1)
+    for i in (0, 7, 15):
+        assert np.array_equal(one.process(ms[i]).energies, e[i])

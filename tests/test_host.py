@@ -1,0 +1,201 @@
+"""Product host side on CPU (no GPU needed): setup tables, steering tables,
+synthesis, validation and the C ABI surface, against the reference oracle
+and the golden fixtures."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, TINY, TINY_SCENE, az181, golden, to_oracle
+
+TABLES = range(5)  # demod_rev, demod_lut, premf_rev, chirp_ref, smooth_decimate_rev
+
+
+def host_ws(sn, cfg):
+    return sn.Workspace(cfg, device=-1)
+
+
+def configs(sn):
+    base = sn.default_pipeline_config(sn.GridKind.horizontal90)
+    return {
+        "h90": base,
+        "box1850": sn.default_pipeline_config(sn.GridKind.box1850),
+        "hemi3000": sn.default_pipeline_config(sn.GridKind.hemisphere3000),
+        "tiny": base.copy(**TINY),
+        "small": base.copy(max_range=1.5),
+        "az181": base.copy(directions=az181(), grid_kind=3),
+        "demod101": base.copy(demod_taps=101),
+        "demod_d8": base.copy(demod_decimation=8, demod_cutoff_hz=110e3),
+        "smooth63": base.copy(smoothing_taps=63, smoothing_cutoff_hz=8e3),
+    }
+
+
+@pytest.mark.parametrize("name", ["h90", "box1850", "hemi3000", "tiny", "small", "az181",
+                                  "demod101", "demod_d8", "smooth63"])
+def test_setup_tables_bit_exact_vs_reference(sn, po, ref, name):
+    cfg = configs(sn)[name]
+    ws = host_ws(sn, cfg)
+    rws = ref.workspace(to_oracle(po, cfg))
+    for t in TABLES:
+        assert np.array_equal(ws.table(t), rws.table(t)), f"table {t}"
+    assert np.array_equal(ws.delay_table(), rws.delay_table())
+    assert np.array_equal(ws.reference_advances(), rws.reference_advances())
+    d = ws.dims
+    for k in ("frames", "demod_samples", "mf_samples", "range_bins", "ref_len", "mf_fft_size",
+              "env_fft_size", "smoothing_len"):
+        assert d[k] == rws.dims[k], k
+    assert d["range_bin_size"] == rws.range_bin_size
+
+
+def test_grids_and_array_match_reference(sn, ref):
+    for k in (0, 1, 2):
+        assert np.array_equal(sn.direction_grid(k), ref.direction_grid(k))
+    for seed in (42, 7, 1234):
+        assert np.array_equal(sn.default_array(seed), ref.default_array(seed))
+
+
+def test_golden_hemi_tables(sn):
+    g = golden("hemi.npz")
+    ws = host_ws(sn, sn.default_pipeline_config(sn.GridKind.hemisphere3000))
+    assert np.array_equal(ws.delay_table(), g["delays"].astype(np.int32))
+    assert np.array_equal(ws.reference_advances(), g["advances"].astype(np.int32))
+    import hashlib
+    assert hashlib.sha256(ws.table(1).tobytes()).hexdigest() == str(g["lut_sha256"])
+
+
+def test_golden_tiny_tables(sn):
+    g = golden("tiny.npz")
+    ws = host_ws(sn, sn.default_pipeline_config().copy(**TINY))
+    for name, t in (("demod_rev", 0), ("demod_lut", 1), ("premf_rev", 2), ("chirp", 3),
+                    ("comp_rev", 4)):
+        assert np.array_equal(ws.table(t), g[name]), name
+    assert np.array_equal(ws.delay_table(), g["delays"])
+
+
+@pytest.mark.parametrize("scene", [
+    dict(reflectors=[], noise_rms=0.0, seed=0),
+    dict(reflectors=[], noise_rms=0.01, seed=3),
+    dict(reflectors=[(1.5, 0.2, 0.0, 0.8), (3.0, -0.4, 0.1, 0.5)], noise_rms=0.01, seed=7),
+    dict(reflectors=[(0.5, -1.2, 0.3, 2.0)], noise_rms=0.0, seed=0),  # clipping regime
+])
+def test_synthesis_bit_exact_vs_reference(sn, po, ref, scene):
+    cfg = sn.default_pipeline_config()
+    m = sn.synthesize_measurement(cfg, sn.Scene([sn.Reflector(*r) for r in scene["reflectors"]],
+                                                scene["noise_rms"], scene["seed"]))
+    want = ref.synthesize(to_oracle(po, cfg), scene["reflectors"], scene["noise_rms"], scene["seed"])
+    assert m.packed.shape == want.shape and np.array_equal(m.packed, want)
+    assert m.channels == 32 and m.frames == 144800 and m.packed.size == 579200
+
+
+def test_synthesis_golden_tiny(sn):
+    g = golden("tiny.npz")
+    cfg = sn.default_pipeline_config().copy(**TINY)
+    m = sn.synthesize_measurement(cfg, sn.Scene([sn.Reflector(*r) for r in TINY_SCENE["reflectors"]],
+                                                TINY_SCENE["noise_rms"], TINY_SCENE["seed"]))
+    assert np.array_equal(m.packed, g["packed"])
+
+
+def test_config_derived_rates(sn):
+    # test_pipeline.cpp:59-74
+    cfg = sn.default_pipeline_config()
+    d = cfg.dims()
+    assert cfg.demod_rate() == pytest.approx(450000.0)
+    assert cfg.mf_rate() == pytest.approx(225000.0)
+    assert cfg.final_rate() == pytest.approx(22500.0)
+    assert d["frames"] % 8 == 0 and d["frames"] % cfg.demod_decimation == 0
+    assert d["demod_samples"] % cfg.pre_mf_decimation == 0
+    assert d["mf_samples"] % cfg.post_envelope_decimation == 0
+    assert d["frames"] / cfg.pdm_rate >= 2 * cfg.max_range / cfg.speed_of_sound + cfg.chirp_duration
+    assert d["range_bins"] >= 1
+    assert d["range_bin_size"] == pytest.approx(343.0 / 45000.0)
+
+
+@pytest.mark.parametrize("change", [
+    dict(max_range=-1.0), dict(demod_taps=256), dict(chirp_f_start=200000.0),
+    dict(directions=np.zeros((0, 2))), dict(max_range=0.001), dict(smoothing_taps=4),
+    dict(speed_of_sound=0.0), dict(pdm_rate=0.0), dict(demod_decimation=0),
+    dict(processing_threads=-1), dict(smoothing_cutoff_hz=200e3), dict(demod_cutoff_hz=3e6),
+])
+def test_config_validation_rejects_nonsense(sn, change):
+    # test_pipeline.cpp:76-93 + pipeline.cpp:60-92
+    cfg = sn.default_pipeline_config().copy(**change)
+    with pytest.raises(sn.ConfigError):
+        sn.Workspace(cfg, device=-1)
+
+
+def test_reference_agrees_on_rejections(sn, po, ref):
+    for change in (dict(max_range=-1.0), dict(demod_taps=256), dict(chirp_f_start=200000.0),
+                   dict(max_range=0.001)):
+        cfg = sn.default_pipeline_config().copy(**change)
+        with pytest.raises(po.OracleError) as e:
+            ref.workspace(to_oracle(po, cfg))
+        assert e.value.status == 1  # ConfigError
+
+
+def test_geometry_and_direction_argument_errors(sn):
+    cfg = sn.default_pipeline_config()
+    bad = cfg.mic_xyz.copy()
+    bad[3] = bad[4]  # two coincident microphones (geometry.cpp:45-55)
+    with pytest.raises(sn.ArgumentError):
+        sn.Workspace(cfg.copy(mic_xyz=bad), device=-1)
+    far = cfg.mic_xyz.copy()
+    far[0, 1] = 0.2  # outside the 5 cm disk
+    with pytest.raises(sn.ArgumentError):
+        sn.Workspace(cfg.copy(mic_xyz=far), device=-1)
+    dirs = cfg.directions.copy()
+    dirs[0, 1] = 2.0  # elevation beyond pi/2 (geometry.cpp:151)
+    with pytest.raises(sn.ArgumentError):
+        sn.Workspace(cfg.copy(directions=dirs), device=-1)
+
+
+def test_process_validation_all_or_error_on_host(sn):
+    # pipeline.cpp:524-540 checks run before any device work (DecodeError),
+    # then a host-only workspace refuses to compute (no CPU fallback).
+    cfg = sn.default_pipeline_config().copy(**TINY)
+    ws = sn.Workspace(cfg, device=-1)
+    m = sn.synthesize_measurement(cfg, sn.Scene())
+    for bad in (dict(channels=16), dict(frames=m.frames - 8), dict(pdm_rate=1e5),
+                dict(packed=m.packed[:-1])):
+        mm = sn.RawMeasurement(**{**m.__dict__, **bad})
+        with pytest.raises(sn.DecodeError):
+            ws.process(mm)
+    with pytest.raises(sn.CudaError):
+        ws.process(m)
+    assert ws.allocation_events() == 0
+
+
+def test_c_abi_exports_every_declared_symbol(sn):
+    header = open(os.path.join(ROOT, "include", "sonarnet_b200.h")).read()
+    declared = set(re.findall(r"\b(sn_[a-z0-9_]+)\s*\(", header))
+    assert len(declared) >= 25
+    lib = ctypes.CDLL(sn.LIB_PATH)
+    missing = [s for s in sorted(declared) if not hasattr(lib, s)]
+    assert not missing, missing
+    out = subprocess.run(["nm", "-D", "--defined-only", sn.LIB_PATH], capture_output=True, text=True)
+    for s in declared:
+        assert re.search(rf"\bT {s}\b", out.stdout), s
+
+
+def test_library_is_sm100a(sn):
+    out = subprocess.run(["cuobjdump", "--list-elf", sn.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_status_names_and_abi_version(sn):
+    L = sn.lib()
+    assert L.sn_abi_version() == 1
+    L.sn_status_name.restype = ctypes.c_char_p
+    assert [L.sn_status_name(i).decode() for i in range(7)] == [
+        "ok", "config", "argument", "decode", "io", "cuda", "internal"]
+
+
+def test_dims_of_standard_configs(sn):
+    d = sn.default_pipeline_config(sn.GridKind.hemisphere3000).dims()
+    assert (d["frames"], d["mf_samples"], d["range_bins"], d["n_directions"]) == (144800, 7240, 655, 3000)
+    t = sn.default_pipeline_config().copy(**TINY).dims()
+    assert (t["frames"], t["range_bins"]) == (13200, 58)
+    s = sn.default_pipeline_config().copy(max_range=1.5).dims()
+    assert (s["frames"], s["mf_samples"], s["range_bins"], s["env_fft_size"]) == (53000, 2650, 196, 4096)
