@@ -267,6 +267,14 @@ __global__ void __launch_bounds__(kThreads) k_beamform_tiles(BeamArgs a) {
 // (first FFT pass, magnitude) instead of being held in shared memory; the
 // envelope is written over the Hilbert output in place.
 // ---------------------------------------------------------------------------
+// per group: max(FFT buffer (M + M/16 complex), D * phase_len reals), even
+__host__ __device__ int envelope_group_reals(int n, int phase_reals) {
+    const int M = n / 2;
+    const int fft = 2 * (M + M / 16);
+    const int r = fft > phase_reals ? fft : phase_reals;
+    return (r + 1) & ~1;
+}
+
 // Composite smoothing/anti-alias FIR evaluated at stride D (the work of
 // detail::strided_filter, filters.hpp:14-39, at pipeline.cpp:466-468), in
 // polyphase form: out[k] = sum_p sum_q rev[q*D + p] * e_p[k + q]. A thread
@@ -275,7 +283,7 @@ __global__ void __launch_bounds__(kThreads) k_beamform_tiles(BeamArgs a) {
 // with the q loop fully unrolled (Q = 45 for the reference's 447 taps / 10),
 // one shared load + one broadcast tap per FIR_R FMAs. Taps beyond comp_len
 // are zero (the tap array is zero-padded to Q*D).
-constexpr int FIR_R = 9;
+constexpr int FIR_R = kFirR;
 constexpr int FIR_Q = 45;
 
 template <typename R>
@@ -333,7 +341,8 @@ __global__ void __launch_bounds__(kThreads * G, 2 / G) k_envelope(EnvArgs a) {
     const int grp = gidx(), tid = gtid();
     R* comp = reinterpret_cast<R*>(smem);
     const int comp_pad = (a.fir_q * a.decim + 1) & ~1;
-    V* bufB = reinterpret_cast<V*>(comp + comp_pad) + (size_t)grp * (M + M / 16);
+    const int group_reals = envelope_group_reals(N, a.decim * a.phase_len);
+    V* bufB = reinterpret_cast<V*>(comp + comp_pad + (size_t)grp * group_reals);
     const R* cr = reinterpret_cast<const R*>(a.comp);
     const V* tw = reinterpret_cast<const V*>(a.tw);
     for (int i = threadIdx.x; i < comp_pad; i += blockDim.x) comp[i] = i < a.comp_len ? cr[i] : (R)0;
@@ -508,10 +517,10 @@ void launch_beamform_tiles(const BeamArgs& a, bool f32, cudaStream_t s) {
     else launch_bf<double>(a, s);
 }
 
-size_t envelope_smem_bytes(int n, int comp_taps_padded, bool f32, int groups) {
+size_t envelope_smem_bytes(int n, int comp_taps_padded, int phase_reals, bool f32, int groups) {
     const size_t rb = f32 ? 4 : 8;
-    const int M = n / 2;
-    return (size_t)((comp_taps_padded + 1) & ~1) * rb + (size_t)groups * (M + M / 16) * 2 * rb;
+    return (size_t)((comp_taps_padded + 1) & ~1) * rb +
+           (size_t)groups * envelope_group_reals(n, phase_reals) * rb;
 }
 
 // Compile-time FFT sizes: N = 2M real points, 32 <= N <= 8192.
@@ -552,10 +561,10 @@ static void env_launch(const EnvArgs& a, int grid, size_t smem, cudaStream_t s) 
 
 void launch_envelope(const EnvArgs& a, bool f32, int grid, cudaStream_t s) {
     if (f32) {
-        const size_t smem = envelope_smem_bytes(a.n, a.fir_q * a.decim, true, kEnvGroupsF32);
+        const size_t smem = envelope_smem_bytes(a.n, a.fir_q * a.decim, a.decim * a.phase_len, true, kEnvGroupsF32);
         SNB_DISPATCH_M(a.n / 2, (env_launch<float, kEnvGroupsF32, MM>(a, grid, smem, s)))
     } else {
-        const size_t smem = envelope_smem_bytes(a.n, a.fir_q * a.decim, false, kEnvGroupsF64);
+        const size_t smem = envelope_smem_bytes(a.n, a.fir_q * a.decim, a.decim * a.phase_len, false, kEnvGroupsF64);
         SNB_DISPATCH_M(a.n / 2, (env_launch<double, kEnvGroupsF64, MM>(a, grid, smem, s)))
     }
 }

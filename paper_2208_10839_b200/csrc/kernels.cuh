@@ -73,6 +73,7 @@ struct EnvArgs {
     int phase_len;           // entries per phase row (>= bins + fir_q + FIR_R)
 };
 
+constexpr int kFirR = 9; // outputs per thread in the polyphase FIR (odd: conflict-free)
 constexpr int kEnvGroupsF64 = 1;
 constexpr int kEnvGroupsF32 = 1;
 
@@ -81,7 +82,8 @@ void launch_premf(const PremfArgs& a, int batch, cudaStream_t s);
 void launch_matched_filter(const MfArgs& a, int batch, size_t smem, cudaStream_t s);
 void launch_beamform_tiles(const BeamArgs& a, bool f32, cudaStream_t s);
 void launch_envelope(const EnvArgs& a, bool f32, int grid, cudaStream_t s);
-size_t envelope_smem_bytes(int n, int comp_taps_padded, bool f32, int groups);
+size_t envelope_smem_bytes(int n, int comp_taps_padded, int phase_reals, bool f32, int groups);
+__host__ __device__ int envelope_group_reals(int n, int phase_reals);
 int envelope_blocks_per_sm(bool f32, int n_fft, size_t smem);
 void launch_rfft_forward(const double* x, double2* X, const double2* tw, int n, size_t smem,
                          cudaStream_t s);

@@ -258,22 +258,17 @@ struct sn_workspace {
         // beamformer time tile: 32 x (T + 2H) samples staged per CTA
         tile = 128;
         {
+            // polyphase FIR rows (fir_polyphase in kernels.cu): every envelope
+            // sample needs a slot and every FIR read stays inside its row
             const int D = plan.cfg.post_envelope_decimation;
+            const int c0 = (int)(plan.comp_rev.size() - 1) / 2;
             fir_q = (int)((plan.comp_rev.size() + D - 1) / D);
-            phase_len = (int)s.bins + fir_q + 16;
-            // the phase rows live in the FFT buffer: D * phase_len <= 2 * (M + M/16)
-            const uint64_t M = s.env_fft / 2;
-            if ((uint64_t)D * phase_len > 2 * (M + M / 16)) {
-                config_error("pipeline: post-envelope FIR does not fit the device envelope buffer");
-            }
-            if (s.mf_len + (plan.comp_rev.size() - 1) / 2 >= (uint64_t)D * phase_len) {
-                phase_len = (int)((s.mf_len + plan.comp_rev.size()) / D + 2);
-                if ((uint64_t)D * phase_len > 2 * (M + M / 16)) {
-                    config_error("pipeline: post-envelope FIR does not fit the device envelope buffer");
-                }
-            }
+            const int groups = (int)((s.bins + kFirR - 1) / kFirR);
+            phase_len = std::max(groups * kFirR + fir_q, (int)((s.mf_len + c0) / D) + 1);
+            phase_len = std::max(phase_len, (int)s.bins + fir_q + 1);
         }
-        dir_smem = envelope_smem_bytes((int)s.env_fft, fir_q * plan.cfg.post_envelope_decimation, f32,
+        dir_smem = envelope_smem_bytes((int)s.env_fft, fir_q * plan.cfg.post_envelope_decimation,
+                                       plan.cfg.post_envelope_decimation * phase_len, f32,
                                        f32 ? kEnvGroupsF32 : kEnvGroupsF64);
         {
             dir_grid = sms * envelope_blocks_per_sm(f32, (int)s.env_fft, dir_smem);
