@@ -158,11 +158,29 @@ __device__ __forceinline__ void stockham_pass(const V* src, V* dst, int M, int n
         const int k = j % ns;
         if (ns > 1) {
             const int step = (M / (ns * RADIX)) * k; // twiddle index per r
+            if constexpr (RADIX == 16) {
+                // w^1, w^2, w^4, w^8 from the table, the other powers by at most
+                // three products (<= 3 roundings): 4 loads instead of 15
+                V w[16];
+                w[1] = tw[(size_t)step * tws];
+                w[2] = tw[(size_t)(2 * step) * tws];
+                w[4] = tw[(size_t)(4 * step) * tws];
+                w[8] = tw[(size_t)(8 * step) * tws];
+                w[3] = cmul(w[1], w[2]);
+                w[5] = cmul(w[1], w[4]);
+                w[6] = cmul(w[2], w[4]);
+                w[7] = cmul(w[3], w[4]);
 #pragma unroll
-            for (int r = 1; r < RADIX; ++r) {
-                V w = tw[(size_t)(step * r) * tws];
-                if (INV) w.y = -w.y;
-                v[r] = cmul(v[r], w);
+                for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
+#pragma unroll
+                for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], INV ? cconj(w[r]) : w[r]);
+            } else {
+#pragma unroll
+                for (int r = 1; r < RADIX; ++r) {
+                    V w = tw[(size_t)(step * r) * tws];
+                    if (INV) w.y = -w.y;
+                    v[r] = cmul(v[r], w);
+                }
             }
         }
         dft_r<RADIX, INV>(v);

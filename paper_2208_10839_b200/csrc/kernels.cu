@@ -3,6 +3,7 @@
 #include "kernels.cuh"
 
 #include <cstdio>
+#include <type_traits>
 
 namespace snb {
 
@@ -249,8 +250,9 @@ __global__ void __launch_bounds__(kThreads) k_beamform_tiles(BeamArgs a) {
                 *reinterpret_cast<float4*>(out + n) = float4{c0 * scale, c1 * scale, c2 * scale, c3 * scale};
             }
         } else {
-            const R v[4] = {c0, c1, c2, c3};
-            for (int k = 0; k < nmax - n; ++k) out[n + k] = v[k] * scale;
+            if (n < nmax) out[n] = c0 * scale;
+            if (n + 1 < nmax) out[n + 1] = c1 * scale;
+            if (n + 2 < nmax) out[n + 2] = c2 * scale;
         }
     }
 }
@@ -283,6 +285,18 @@ __host__ __device__ int envelope_group_reals(int n, int phase_reals) {
 // with the q loop fully unrolled (Q = 45 for the reference's 447 taps / 10),
 // one shared load + one broadcast tap per FIR_R FMAs. Taps beyond comp_len
 // are zero (the tap array is zero-padded to Q*D).
+// |b + iH(b)|. FP64: rsqrt seed from the SFU (~22 bits), one Newton step on
+// the reciprocal root (~44 bits) and one on the root itself (<= 1 ulp),
+// instead of the correctly rounded library sequence; FP32: sqrtf.
+__device__ __forceinline__ double fast_sqrt(double x) {
+    if (!(x > 1e-30 && x < 1e30)) return sqrt(x);
+    double r = (double)rsqrtf((float)x);
+    r = r * fma(-0.5 * x, r * r, 1.5);
+    const double s = x * r;
+    return fma(0.5 * r, fma(-s, s, x), s);
+}
+__device__ __forceinline__ float fast_sqrt(float x) { return sqrtf(x); }
+
 constexpr int FIR_R = kFirR;
 constexpr int FIR_Q = 45;
 
@@ -374,24 +388,38 @@ __global__ void __launch_bounds__(kThreads * G, 2 / G) k_envelope(EnvArgs a) {
             if (n < L) {
                 const R h = env[n + 2 * (n >> 5)];
                 const R bv = src[n];
-                ev[i] = sqrt(bv * bv + h * h);
+                ev[i] = fast_sqrt(bv * bv + h * h);
             }
         }
         gsync();
         R* ph = env; // phases: D rows of U entries
+        {
+            // t = n + c0 -> (p, u) = (t mod D, t / D), stepped without division
+            const int D = a.decim;
+            const int du = kGroupThreads / D, dp = kGroupThreads - du * D;
+            int t0 = tid + c0;
+            int u = t0 / D, pp = t0 - u * D;
 #pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int n = tid + i * kGroupThreads;
-            if (n < L) {
-                const int t = n + c0;
-                ph[(t % a.decim) * a.phase_len + t / a.decim] = ev[i];
+            for (int i = 0; i < NV; ++i) {
+                const int n = tid + i * kGroupThreads;
+                if (n < L) ph[pp * a.phase_len + u] = ev[i];
+                u += du;
+                pp += dp;
+                if (pp >= D) {
+                    pp -= D;
+                    ++u;
+                }
             }
-        }
-        // zero the phase slots whose sample lies outside [0, L)
-        for (int idx = tid; idx < a.decim * a.phase_len; idx += kGroupThreads) {
-            const int p = idx / a.phase_len, u = idx - p * a.phase_len;
-            const int64_t n = (int64_t)u * a.decim - c0 + p;
-            if (n < 0 || n >= L) ph[idx] = 0;
+            // zero the slots whose sample lies outside [0, L): per phase row p,
+            // u < ceil((c0 - p) / D) and u >= ceil((L + c0 - p) / D)
+            if (tid < D) {
+                const int p = tid;
+                const int lo = c0 >= p ? (c0 - p + D - 1) / D : 0;
+                const int hi = (int)((L + c0 - p + D - 1) / D);
+                R* row = ph + p * a.phase_len;
+                for (int k = 0; k < lo; ++k) row[k] = 0;
+                for (int k = hi; k < a.phase_len; ++k) row[k] = 0;
+            }
         }
         gsync();
         float* eo = a.energy + ((size_t)b * a.n_dirs + a.order[slot]) * a.bins;

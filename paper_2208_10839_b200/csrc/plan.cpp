@@ -4,6 +4,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -391,27 +392,45 @@ Plan make_plan(const sn_pipeline_config& cin) {
         }
         p.advances[d] = static_cast<int32_t>(std::llround(-lo * s.mf_rate));
     }
-    // Direction schedule: sort directions along a Morton curve over the
-    // boresight-plane components (u_y, u_z) of their unit vectors so that the
-    // 32 directions a warp beamforms together have nearby per-channel shifts
-    // (a shared-memory load then serves all 32 lanes from one or two
-    // 128-byte wavefronts).
+    // Direction schedule: recursive median bisection (k-d tree) of the
+    // boresight-plane components (u_y, u_z) of the unit vectors into leaves of
+    // kClusterDirs directions; leaves are laid out consecutively, so the 8
+    // directions a beamformer warp processes together are angular neighbours
+    // with per-channel shift spreads of a few samples. Scheduling only: every
+    // direction is independent (pipeline.cpp:225-226).
     {
-        std::vector<std::pair<uint64_t, int32_t>> keyed(s.n_dirs);
+        std::vector<double> uy(s.n_dirs), uz(s.n_dirs);
         for (uint64_t d = 0; d < s.n_dirs; ++d) {
             const V3 u = unit_vector(p.directions[2 * d], p.directions[2 * d + 1]);
-            auto q = [](double v) {
-                const double t = std::clamp((v + 1.0) * 0.5, 0.0, 1.0);
-                return static_cast<uint32_t>(t * 65535.0 + 0.5);
-            };
-            const uint32_t a = q(u.y), b = q(u.z);
-            uint64_t key = 0;
-            for (int bit = 15; bit >= 0; --bit) {
-                key = (key << 2) | (((b >> bit) & 1u) << 1) | ((a >> bit) & 1u);
-            }
-            keyed[d] = {key, static_cast<int32_t>(d)};
+            uy[d] = u.y;
+            uz[d] = u.z;
         }
-        std::stable_sort(keyed.begin(), keyed.end());
+        std::vector<int32_t> idx(s.n_dirs);
+        std::iota(idx.begin(), idx.end(), 0);
+        std::vector<int32_t> leaves;
+        leaves.reserve(s.n_dirs);
+        auto split = [&](auto&& self, int32_t* b, int32_t* e) -> void {
+            const int64_t n = e - b;
+            if (n <= kClusterDirs) {
+                leaves.insert(leaves.end(), b, e);
+                return;
+            }
+            double ylo = 1e9, yhi = -1e9, zlo = 1e9, zhi = -1e9;
+            for (int32_t* q = b; q != e; ++q) {
+                ylo = std::min(ylo, uy[*q]);
+                yhi = std::max(yhi, uy[*q]);
+                zlo = std::min(zlo, uz[*q]);
+                zhi = std::max(zhi, uz[*q]);
+            }
+            const std::vector<double>& key = (yhi - ylo >= zhi - zlo) ? uy : uz;
+            std::stable_sort(b, e, [&](int32_t x, int32_t y) { return key[x] < key[y]; });
+            const int64_t nl = kClusterDirs * ((n + 2 * kClusterDirs - 1) / (2 * kClusterDirs));
+            self(self, b, b + nl);
+            self(self, b + nl, e);
+        };
+        split(split, idx.data(), idx.data() + idx.size());
+        std::vector<std::pair<uint64_t, int32_t>> keyed(s.n_dirs);
+        for (uint64_t k = 0; k < s.n_dirs; ++k) keyed[k] = {k, leaves[k]};
         p.order.resize(s.n_dirs);
         p.shifts.resize(s.n_dirs * kCh);
         int32_t halo = 0;

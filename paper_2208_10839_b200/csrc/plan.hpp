@@ -55,6 +55,8 @@ struct Plan {
     int32_t halo = 0;                 // max |shift| over all directions/channels
 };
 
+constexpr int kClusterDirs = 8; // k-d leaf size of the direction schedule
+
 // Validates (pipeline.cpp:60-92; geometry.cpp:27-57 invariants; Direction
 // ranges geometry.cpp:146-155) and derives every table. Throws Error.
 Plan make_plan(const sn_pipeline_config& cfg);

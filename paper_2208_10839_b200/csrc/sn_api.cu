@@ -100,6 +100,7 @@ struct sn_workspace {
     void* d_beams = nullptr;
     int32_t* d_order = nullptr;
     int32_t* d_shifts_slot = nullptr;
+
     float* d_energy = nullptr;
     double* d_lut = nullptr;
     double* d_premf = nullptr;
@@ -138,7 +139,7 @@ struct sn_workspace {
             if (e) cudaEventDestroy(e);
         }
         for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
-                        (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot, (void*)d_energy, (void*)d_lut, (void*)d_premf,
+                        (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot,  (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
                         (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32}) {
             if (p) cudaFree(p);
@@ -184,6 +185,7 @@ struct sn_workspace {
         d_shifts_slot = dmalloc<int32_t>(s.n_dirs * kCh, n);
         upload(d_order, plan.order, stream);
         upload(d_shifts_slot, plan.shifts, stream);
+
         d_energy = dmalloc<float>(B * energy_per, n);
         d_lut = dmalloc<double>(plan.demod_lut.size(), n);
         d_premf = dmalloc<double>(plan.premf_rev.size(), n);
