@@ -289,8 +289,9 @@ __host__ __device__ int envelope_group_reals(int n, int phase_reals) {
 // the reciprocal root (~44 bits) and one on the root itself (<= 1 ulp),
 // instead of the correctly rounded library sequence; FP32: sqrtf.
 __device__ __forceinline__ double fast_sqrt(double x) {
-    if (!(x > 1e-30 && x < 1e30)) return sqrt(x);
-    double r = (double)rsqrtf((float)x);
+    // branch-free: the seed is clamped to the float range; x == 0 gives 0
+    const float xf = fminf(fmaxf((float)x, 1.17549435e-38f), 3.0e38f);
+    double r = (double)rsqrtf(xf);
     r = r * fma(-0.5 * x, r * r, 1.5);
     const double s = x * r;
     return fma(0.5 * r, fma(-s, s, x), s);
@@ -381,33 +382,40 @@ __global__ void __launch_bounds__(kThreads * G, 2 / G) k_envelope(EnvArgs a) {
         // [0, L)) that the polyphase FIR below reads with unit stride.
         constexpr int NV = (2 * M + kGroupThreads - 1) / kGroupThreads;
         R ev[NV];
+        // all beam loads first (one batch of independent L2 reads), then the
+        // shared Hilbert values and the roots, in place in the same registers
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             const int n = tid + i * kGroupThreads;
-            ev[i] = 0;
+            ev[i] = n < L ? __ldg(src + n) : (R)0;
+        }
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int n = tid + i * kGroupThreads;
             if (n < L) {
                 const R h = env[n + 2 * (n >> 5)];
-                const R bv = src[n];
-                ev[i] = fast_sqrt(bv * bv + h * h);
+                ev[i] = fast_sqrt(ev[i] * ev[i] + h * h);
             }
         }
         gsync();
         R* ph = env; // phases: D rows of U entries
         {
-            // t = n + c0 -> (p, u) = (t mod D, t / D), stepped without division
-            const int D = a.decim;
+            // t = n + c0 -> slot (t mod D) * phase_len + t / D, stepped by
+            // kGroupThreads samples without division
+            const int D = a.decim, PL = a.phase_len;
             const int du = kGroupThreads / D, dp = kGroupThreads - du * D;
-            int t0 = tid + c0;
-            int u = t0 / D, pp = t0 - u * D;
+            const int t0 = tid + c0;
+            int pp = t0 % D;
+            int addr = pp * PL + t0 / D;
+            const int step = du + dp * PL, wrap = 1 - D * PL;
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
-                const int n = tid + i * kGroupThreads;
-                if (n < L) ph[pp * a.phase_len + u] = ev[i];
-                u += du;
+                if (tid + i * kGroupThreads < L) ph[addr] = ev[i];
+                addr += step;
                 pp += dp;
                 if (pp >= D) {
                     pp -= D;
-                    ++u;
+                    addr += wrap;
                 }
             }
             // zero the slots whose sample lies outside [0, L): per phase row p,

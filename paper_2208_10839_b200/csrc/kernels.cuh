@@ -73,7 +73,7 @@ struct EnvArgs {
     int phase_len;           // entries per phase row (>= bins + fir_q + FIR_R)
 };
 
-constexpr int kFirR = 9; // outputs per thread in the polyphase FIR (odd: conflict-free)
+constexpr int kFirR = 3; // outputs per thread in the polyphase FIR (odd: conflict-free)
 constexpr int kEnvGroupsF64 = 1;
 constexpr int kEnvGroupsF32 = 1;
 
