@@ -26,7 +26,8 @@ from typing import Iterable, List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsonarnet_b200.so")
+# SNB_LIB: developer override (A/B builds of the same sources); default in-tree build
+LIB_PATH = os.environ.get("SNB_LIB") or os.path.join(_HERE, "_lib", "libsonarnet_b200.so")
 
 __all__ = [
     "GridKind", "Precision", "PipelineConfig", "RawMeasurement", "AcousticImage", "Reflector",

@@ -3,6 +3,10 @@
 #include "kernels.cuh"
 
 #include <cstdio>
+
+#ifndef SNB_ENV_MINB
+#define SNB_ENV_MINB 2 // envelope CTAs per SM the register budget is sized for
+#endif
 #include <type_traits>
 
 namespace snb {
@@ -269,22 +273,16 @@ __global__ void __launch_bounds__(kThreads) k_beamform_tiles(BeamArgs a) {
 // (first FFT pass, magnitude) instead of being held in shared memory; the
 // envelope is written over the Hilbert output in place.
 // ---------------------------------------------------------------------------
-// per group: max(FFT buffer (M + M/16 complex), D * phase_len reals), even
+// per group: max(FFT buffer (M + M/16 complex), D * phase_len reals + the FIR
+// half-sum scratch), even
 __host__ __device__ int envelope_group_reals(int n, int phase_reals) {
     const int M = n / 2;
     const int fft = 2 * (M + M / 16);
-    const int r = fft > phase_reals ? fft : phase_reals;
+    const int ph = phase_reals + kFirScratch;
+    const int r = fft > ph ? fft : ph;
     return (r + 1) & ~1;
 }
 
-// Composite smoothing/anti-alias FIR evaluated at stride D (the work of
-// detail::strided_filter, filters.hpp:14-39, at pipeline.cpp:466-468), in
-// polyphase form: out[k] = sum_p sum_q rev[q*D + p] * e_p[k + q]. A thread
-// owns FIR_R consecutive outputs (odd, so a warp's loads of one phase row are
-// bank-conflict free); for each phase it slides a register window over e_p
-// with the q loop fully unrolled (Q = 45 for the reference's 447 taps / 10),
-// one shared load + one broadcast tap per FIR_R FMAs. Taps beyond comp_len
-// are zero (the tap array is zero-padded to Q*D).
 // |b + iH(b)|. FP64: rsqrt seed from the SFU (~22 bits), one Newton step on
 // the reciprocal root (~44 bits) and one on the root itself (<= 1 ulp),
 // instead of the correctly rounded library sequence; FP32: sqrtf.
@@ -298,44 +296,69 @@ __device__ __forceinline__ double fast_sqrt(double x) {
 }
 __device__ __forceinline__ float fast_sqrt(float x) { return sqrtf(x); }
 
-constexpr int FIR_R = kFirR;
-constexpr int FIR_Q = 45;
+// Composite smoothing/anti-alias FIR evaluated at stride D (the work of
+// detail::strided_filter, filters.hpp:14-39, at pipeline.cpp:466-468), in
+// polyphase form: out[k] = sum_p sum_q rev[q*D + p] * e_p[k + q], e_p read
+// from the decimation-phase rows `ph` (row p at ph + p * phase_len).
+//
+// Fast path (D = 10, Q = 45): warps 0-3 of the group sum phases 0-4, warps 4-7
+// phases 5-9, for the same kFirR consecutive outputs per thread; a register
+// window slides over the row (one LDS per kFirR FMAs, conflict-free for odd
+// kFirR) and every tap is a compile-time index into the kernel-parameter
+// array, i.e. a constant-bank operand of the FMA. The upper half hands its
+// partial sums to the lower half through `red`.
+template <int H, typename R>
+__device__ __forceinline__ void fir_half(const R* ph, const FirTaps<R>& taps, int phase_len, int k0,
+                                         R (&acc)[kFirR]) {
+#pragma unroll
+    for (int pp = 0; pp < kFirD / 2; ++pp) {
+        constexpr int P0 = H * (kFirD / 2);
+        const R* row = ph + (P0 + pp) * phase_len + k0;
+        R w[kFirR + kFirQ];
+#pragma unroll
+        for (int r = 0; r < kFirR; ++r) w[r] = row[r];
+#pragma unroll
+        for (int q = 0; q < kFirQ; ++q) {
+            if (q + 1 < kFirQ) w[kFirR + q] = row[kFirR + q]; // used from step q + 1 on
+            const R c = taps.c[(P0 + pp) * kFirQ + q];
+#pragma unroll
+            for (int r = 0; r < kFirR; ++r) acc[r] = fma(c, w[q + r], acc[r]);
+        }
+    }
+}
 
 template <typename R>
-__device__ __forceinline__ void fir_polyphase(const R* ph, const R* comp, const EnvArgs& a,
-                                              float* eo) {
+__device__ __forceinline__ void fir_polyphase(const R* ph, const R* comp, const FirTaps<R>& taps,
+                                              const EnvArgs& a, float* eo) {
     const int tid = gtid();
-    const int groups = (int)((a.bins + FIR_R - 1) / FIR_R);
-    if (a.fir_q == FIR_Q) {
-        for (int g = tid; g < groups; g += kGroupThreads) {
-            const int k0 = g * FIR_R;
-            R acc[FIR_R];
+    if (a.fir_fast) {
+        const int h = tid >> 7, g = tid & 127;
+        const int groups = (int)((a.bins + kFirR - 1) / kFirR);
+        const int k0 = g * kFirR;
+        R acc[kFirR];
 #pragma unroll
-            for (int r = 0; r < FIR_R; ++r) acc[r] = 0;
-            for (int p = 0; p < a.decim; ++p) {
-                const R* row = ph + p * a.phase_len + k0;
-                const R* tp = comp + p;
-                R w[FIR_R + FIR_Q];
+        for (int r = 0; r < kFirR; ++r) acc[r] = 0;
+        R* red = const_cast<R*>(ph) + kFirD * a.phase_len;
+        if (g < groups) {
+            if (h == 0) fir_half<0>(ph, taps, a.phase_len, k0, acc);
+            else fir_half<1>(ph, taps, a.phase_len, k0, acc);
+            if (h == 1) {
 #pragma unroll
-                for (int r = 0; r < FIR_R; ++r) w[r] = row[r];
-#pragma unroll
-                for (int q = 0; q < FIR_Q; ++q) {
-                    w[FIR_R + q] = row[FIR_R + q];
-                    const R c = tp[q * a.decim];
-#pragma unroll
-                    for (int r = 0; r < FIR_R; ++r) acc[r] = fma(c, w[q + r], acc[r]);
-                }
+                for (int r = 0; r < kFirR; ++r) red[k0 + r] = acc[r];
             }
+        }
+        gsync();
+        if (h == 0 && g < groups) {
 #pragma unroll
-            for (int r = 0; r < FIR_R; ++r) {
+            for (int r = 0; r < kFirR; ++r) {
                 if (k0 + r < a.bins) {
-                    const float v = (float)acc[r];
+                    const float v = (float)(acc[r] + red[k0 + r]);
                     eo[k0 + r] = v > 0.0f ? v : 0.0f;
                 }
             }
         }
     } else {
-        // generic tap count: plain polyphase loops
+        // generic decimation / tap count: plain polyphase loops, taps in smem
         for (int64_t k = tid; k < a.bins; k += kGroupThreads) {
             R acc = 0;
             for (int p = 0; p < a.decim; ++p) {
@@ -349,7 +372,7 @@ __device__ __forceinline__ void fir_polyphase(const R* ph, const R* comp, const 
 }
 
 template <typename R, int G, int M>
-__global__ void __launch_bounds__(kThreads * G, 2 / G) k_envelope(EnvArgs a) {
+__global__ void __launch_bounds__(kThreads * G, SNB_ENV_MINB / G) k_envelope(EnvArgs a, FirTaps<R> taps) {
     using V = typename Cx<R>::T;
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int N = 2 * M;
@@ -431,7 +454,7 @@ __global__ void __launch_bounds__(kThreads * G, 2 / G) k_envelope(EnvArgs a) {
         }
         gsync();
         float* eo = a.energy + ((size_t)b * a.n_dirs + a.order[slot]) * a.bins;
-        fir_polyphase<R>(ph, comp, a, eo);
+        fir_polyphase<R>(ph, comp, taps, a, eo);
         gsync();
     }
 }
@@ -590,18 +613,19 @@ int envelope_blocks_per_sm(bool f32, int n_fft, size_t smem) {
 }
 
 template <typename R, int G, int M>
-static void env_launch(const EnvArgs& a, int grid, size_t smem, cudaStream_t s) {
+static void env_launch(const EnvArgs& a, const FirTaps<R>& taps, int grid, size_t smem, cudaStream_t s) {
     set_smem((const void*)k_envelope<R, G, M>, smem);
-    k_envelope<R, G, M><<<grid, kThreads * G, smem, s>>>(a);
+    k_envelope<R, G, M><<<grid, kThreads * G, smem, s>>>(a, taps);
 }
 
-void launch_envelope(const EnvArgs& a, bool f32, int grid, cudaStream_t s) {
+void launch_envelope(const EnvArgs& a, const FirTaps<float>& t32, const FirTaps<double>& t64, bool f32,
+                     int grid, cudaStream_t s) {
     if (f32) {
         const size_t smem = envelope_smem_bytes(a.n, a.fir_q * a.decim, a.decim * a.phase_len, true, kEnvGroupsF32);
-        SNB_DISPATCH_M(a.n / 2, (env_launch<float, kEnvGroupsF32, MM>(a, grid, smem, s)))
+        SNB_DISPATCH_M(a.n / 2, (env_launch<float, kEnvGroupsF32, MM>(a, t32, grid, smem, s)))
     } else {
         const size_t smem = envelope_smem_bytes(a.n, a.fir_q * a.decim, a.decim * a.phase_len, false, kEnvGroupsF64);
-        SNB_DISPATCH_M(a.n / 2, (env_launch<double, kEnvGroupsF64, MM>(a, grid, smem, s)))
+        SNB_DISPATCH_M(a.n / 2, (env_launch<double, kEnvGroupsF64, MM>(a, t64, grid, smem, s)))
     }
 }
 

@@ -71,9 +71,19 @@ struct EnvArgs {
     int n, comp_len, decim, batch;
     int fir_q;               // ceil(comp_len / decim): taps per phase
     int phase_len;           // entries per phase row (>= bins + fir_q + FIR_R)
+    int fir_fast;            // decim == kFirD, fir_q == kFirQ, bins <= 128 * kFirR
 };
 
-constexpr int kFirR = 3; // outputs per thread in the polyphase FIR (odd: conflict-free)
+// Polyphase smoothing FIR fast path (the reference's default composite
+// filter: 447 taps at stride 10 -> 10 phases x 45 taps): every thread owns
+// kFirR consecutive outputs (odd: bank-conflict free) over one half of the
+// phases; taps travel in the kernel parameters so every FMA takes its tap as
+// a constant-bank operand (no shared-memory tap loads).
+constexpr int kFirR = 7;
+constexpr int kFirD = 10, kFirQ = 45;              // decimation, taps per phase
+constexpr int kFirTaps = kFirD * kFirQ;            // 450 (zero-padded)
+constexpr int kFirScratch = 128 * kFirR;           // half-sum exchange (reals)
+template <typename R> struct FirTaps { R c[kFirTaps]; }; // c[p * kFirQ + q] = comp[q * kFirD + p]
 constexpr int kEnvGroupsF64 = 1;
 constexpr int kEnvGroupsF32 = 1;
 
@@ -81,7 +91,8 @@ void launch_demod(const DemodArgs& a, int grid_x, size_t smem, cudaStream_t s);
 void launch_premf(const PremfArgs& a, int batch, cudaStream_t s);
 void launch_matched_filter(const MfArgs& a, int batch, size_t smem, cudaStream_t s);
 void launch_beamform_tiles(const BeamArgs& a, bool f32, cudaStream_t s);
-void launch_envelope(const EnvArgs& a, bool f32, int grid, cudaStream_t s);
+void launch_envelope(const EnvArgs& a, const FirTaps<float>& t32, const FirTaps<double>& t64, bool f32,
+                     int grid, cudaStream_t s);
 size_t envelope_smem_bytes(int n, int comp_taps_padded, int phase_reals, bool f32, int groups);
 __host__ __device__ int envelope_group_reals(int n, int phase_reals);
 int envelope_blocks_per_sm(bool f32, int n_fft, size_t smem);

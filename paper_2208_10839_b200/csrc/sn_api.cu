@@ -90,6 +90,11 @@ struct sn_workspace {
     int device = -1;
     uint64_t max_batch = 1;
     cudaStream_t stream = nullptr;
+    // host path: copies run on their own streams so that chunk j+1's H2D and
+    // chunk j-1's D2H overlap chunk j's kernels
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    static constexpr int kMaxChunks = 8;
+    cudaEvent_t ev_in[kMaxChunks] = {}, ev_done[kMaxChunks] = {};
     bool f32 = false;
     // device buffers
     uint8_t* d_packed = nullptr;
@@ -117,7 +122,9 @@ struct sn_workspace {
     DemodArgs demod{};
     int demod_grid = 0;
     size_t demod_smem = 0, mf_smem = 0, dir_smem = 0;
-    int dir_grid = 0, halo = 0, tile = 0, fir_q = 0, phase_len = 0;
+    int dir_grid = 0, halo = 0, tile = 0, fir_q = 0, phase_len = 0, fir_fast = 0;
+    FirTaps<double> taps64{};
+    FirTaps<float> taps32{};
     uint64_t packed_bytes = 0, energy_per = 0, lp = 0;
     uint64_t alloc_events = 0, device_allocs = 0, last_launches = 0;
     // optional per-stage timing (events on the launching stream)
@@ -138,6 +145,12 @@ struct sn_workspace {
         for (cudaEvent_t e : ev) {
             if (e) cudaEventDestroy(e);
         }
+        for (int j = 0; j < kMaxChunks; ++j) {
+            if (ev_in[j]) cudaEventDestroy(ev_in[j]);
+            if (ev_done[j]) cudaEventDestroy(ev_done[j]);
+        }
+        if (s_h2d) cudaStreamDestroy(s_h2d);
+        if (s_d2h) cudaStreamDestroy(s_d2h);
         for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
                         (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot,  (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
@@ -163,6 +176,12 @@ struct sn_workspace {
         if (s.mf_fft < 32 || s.env_fft < 32) config_error("pipeline: processed window too short for the device FFT");
         DeviceGuard g(device);
         ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+        for (int j = 0; j < kMaxChunks; ++j) {
+            ck(cudaEventCreateWithFlags(&ev_in[j], cudaEventDisableTiming), "cudaEventCreate");
+            ck(cudaEventCreateWithFlags(&ev_done[j], cudaEventDisableTiming), "cudaEventCreate");
+        }
         packed_bytes = static_cast<uint64_t>(kCh) * s.frames / 8;
         energy_per = s.n_dirs * s.bins;
         const uint64_t B = max_batch;
@@ -268,6 +287,17 @@ struct sn_workspace {
             const int groups = (int)((s.bins + kFirR - 1) / kFirR);
             phase_len = std::max(groups * kFirR + fir_q, (int)((s.mf_len + c0) / D) + 1);
             phase_len = std::max(phase_len, (int)s.bins + fir_q + 1);
+            fir_fast = D == kFirD && fir_q == kFirQ && groups <= 128;
+            if (fir_fast) {
+                for (int p = 0; p < kFirD; ++p) {
+                    for (int q = 0; q < kFirQ; ++q) {
+                        const size_t j = (size_t)q * kFirD + p;
+                        const double v = j < plan.comp_rev.size() ? plan.comp_rev[j] : 0.0;
+                        taps64.c[p * kFirQ + q] = v;
+                        taps32.c[p * kFirQ + q] = (float)v;
+                    }
+                }
+            }
         }
         dir_smem = envelope_smem_bytes((int)s.env_fft, fir_q * plan.cfg.post_envelope_decimation,
                                        plan.cfg.post_envelope_decimation * phase_len, f32,
@@ -325,7 +355,8 @@ struct sn_workspace {
         ea.batch = (int)count;
         ea.fir_q = fir_q;
         ea.phase_len = phase_len;
-        launch_envelope(ea, f32, dir_grid, s);
+        ea.fir_fast = fir_fast;
+        launch_envelope(ea, taps32, taps64, f32, dir_grid, s);
         if (profiling) cudaEventRecord(ev[5], s);
         ck(cudaGetLastError(), "kernel launch");
         last_launches = 5;
@@ -362,9 +393,11 @@ struct sn_workspace {
     }
 
     // Host path: H2D of every capture, the device pipeline, D2H of the
-    // energyscapes, one stream synchronisation. Caller buffers that are
-    // page-locked are DMA'd directly; pageable ones go through the
-    // workspace's pinned staging buffers.
+    // energyscapes, one synchronisation per max_batch block. A block is cut
+    // into up to kMaxChunks chunks pipelined over three streams (H2D, kernels,
+    // D2H) so only the first chunk's upload and the last chunk's download are
+    // exposed. Caller buffers that are page-locked are DMA'd directly;
+    // pageable ones go through the workspace's pinned staging buffers.
     void process_host(const sn_raw_measurement* ms, uint64_t count, float* out) {
         for (uint64_t i = 0; i < count; ++i) validate(ms[i]); // all-or-error
         require_device();
@@ -373,22 +406,30 @@ struct sn_workspace {
         uint64_t done = 0;
         while (done < count) {
             const uint64_t c = std::min(max_batch, count - done);
-            for (uint64_t i = 0; i < c; ++i) {
-                const uint8_t* src = ms[done + i].packed;
-                if (is_pinned(src)) {
+            const uint64_t nch = std::min<uint64_t>(c, kMaxChunks);
+            uint64_t off = 0;
+            for (uint64_t j = 0; j < nch; ++j) {
+                const uint64_t k = c / nch + (j < c % nch ? 1 : 0); // captures in chunk j
+                for (uint64_t i = off; i < off + k; ++i) {
+                    const uint8_t* src = ms[done + i].packed;
+                    if (!is_pinned(src)) {
+                        std::memcpy(h_in + i * packed_bytes, src, packed_bytes);
+                        src = h_in + i * packed_bytes;
+                    }
                     ck(cudaMemcpyAsync(d_packed + i * packed_bytes, src, packed_bytes,
-                                       cudaMemcpyHostToDevice, stream), "H2D");
-                } else {
-                    std::memcpy(h_in + i * packed_bytes, src, packed_bytes);
-                    ck(cudaMemcpyAsync(d_packed + i * packed_bytes, h_in + i * packed_bytes,
-                                       packed_bytes, cudaMemcpyHostToDevice, stream), "H2D");
+                                       cudaMemcpyHostToDevice, s_h2d), "H2D");
                 }
+                ck(cudaEventRecord(ev_in[j], s_h2d), "event");
+                ck(cudaStreamWaitEvent(stream, ev_in[j], 0), "wait");
+                enqueue(d_packed + off * packed_bytes, k, d_energy + off * energy_per, stream);
+                ck(cudaEventRecord(ev_done[j], stream), "event");
+                ck(cudaStreamWaitEvent(s_d2h, ev_done[j], 0), "wait");
+                float* dst = (out_pinned ? out + done * energy_per : h_out) + off * energy_per;
+                ck(cudaMemcpyAsync(dst, d_energy + off * energy_per, k * energy_per * sizeof(float),
+                                   cudaMemcpyDeviceToHost, s_d2h), "D2H");
+                off += k;
             }
-            enqueue(d_packed, c, d_energy, stream);
-            float* dst = out_pinned ? out + done * energy_per : h_out;
-            ck(cudaMemcpyAsync(dst, d_energy, c * energy_per * sizeof(float), cudaMemcpyDeviceToHost,
-                               stream), "D2H");
-            ck(cudaStreamSynchronize(stream), "process sync");
+            ck(cudaStreamSynchronize(s_d2h), "process sync");
             if (!out_pinned) std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
             done += c;
         }
