@@ -137,14 +137,43 @@ __device__ __forceinline__ void dft_r(V* x) {
     else dft2<INV>(x[0], x[1]);
 }
 
+// Twiddle sources. A pass of radix R at sub-transform length ns needs
+// w(k, e) = e^{-2 pi i step e / M}, step = (M / (ns R)) k; the real split/merge
+// needs h(k) = e^{-2 pi i k / N}, N = 2M, k in [0, M].
+//   TwGlobal: one table e^{-2 pi i k / Nt} in global memory, read at stride
+//             tws (Nt = tws * N for a table shared with a larger size).
+//   TwShared: compact per-pass tables in shared memory for M = 4096
+//             (radix-16 passes at ns = 16 and 256 need e in {1,2,4,8} only)
+//             and a two-level table for h(k) = A[k >> 6] * B[k & 63].
+template <typename V> struct TwGlobal {
+    const V* __restrict__ tw;
+    int tws;
+    __device__ __forceinline__ V w(int M, int ns, int R, int k, int e) const {
+        return tw[(size_t)((M / (ns * R)) * k * e) * tws];
+    }
+    __device__ __forceinline__ V h(int k) const { return tw[k]; }
+};
+
+constexpr int kTwSharedM = 4096;
+constexpr int kTwSharedCount = 16 * 4 + 256 * 4 + 65 + 64; // complex entries
+template <typename V> struct TwShared {
+    const V* t; // [t16: 16x4][t256: 256x4][A: 65][B: 64]
+    __device__ __forceinline__ V w(int, int ns, int, int k, int e) const {
+        const int le = e == 1 ? 0 : e == 2 ? 1 : e == 4 ? 2 : 3;
+        return ns == 16 ? t[k * 4 + le] : t[64 + k * 4 + le];
+    }
+    __device__ __forceinline__ V h(int k) const {
+        const V a = t[64 + 1024 + (k >> 6)], b = t[64 + 1024 + 65 + (k & 63)];
+        return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+    }
+};
+
 // One Stockham pass: radix RADIX, current sub-transform length ns.
 // src element i at src[SRC_PADDED ? pad16(i) : i]; dst always padded.
-// twM = e^{-2 pi i k / M} table, stride `tws` (table may be for a larger size).
 // In place (src == dst) is allowed: every thread loads all of its inputs
 // before a CTA barrier, then stores.
-template <int RADIX, bool INV, bool SRC_PADDED, typename V>
-__device__ __forceinline__ void stockham_pass(const V* src, V* dst, int M, int ns,
-                                              const V* __restrict__ tw, int tws) {
+template <int RADIX, bool INV, bool SRC_PADDED, typename V, typename TW>
+__device__ __forceinline__ void stockham_pass(const V* src, V* dst, int M, int ns, const TW& tw) {
     const int nj = M / RADIX;
     const int j = gtid();
     V v[RADIX];
@@ -157,15 +186,14 @@ __device__ __forceinline__ void stockham_pass(const V* src, V* dst, int M, int n
         }
         const int k = j % ns;
         if (ns > 1) {
-            const int step = (M / (ns * RADIX)) * k; // twiddle index per r
             if constexpr (RADIX == 16) {
                 // w^1, w^2, w^4, w^8 from the table, the other powers by at most
                 // three products (<= 3 roundings): 4 loads instead of 15
                 V w[16];
-                w[1] = tw[(size_t)step * tws];
-                w[2] = tw[(size_t)(2 * step) * tws];
-                w[4] = tw[(size_t)(4 * step) * tws];
-                w[8] = tw[(size_t)(8 * step) * tws];
+                w[1] = tw.w(M, ns, 16, k, 1);
+                w[2] = tw.w(M, ns, 16, k, 2);
+                w[4] = tw.w(M, ns, 16, k, 4);
+                w[8] = tw.w(M, ns, 16, k, 8);
                 w[3] = cmul(w[1], w[2]);
                 w[5] = cmul(w[1], w[4]);
                 w[6] = cmul(w[2], w[4]);
@@ -177,7 +205,7 @@ __device__ __forceinline__ void stockham_pass(const V* src, V* dst, int M, int n
             } else {
 #pragma unroll
                 for (int r = 1; r < RADIX; ++r) {
-                    V w = tw[(size_t)(step * r) * tws];
+                    V w = tw.w(M, ns, RADIX, k, r);
                     if (INV) w.y = -w.y;
                     v[r] = cmul(v[r], w);
                 }
@@ -198,14 +226,14 @@ __device__ __forceinline__ void stockham_pass(const V* src, V* dst, int M, int n
 // Full M-point complex FFT, M a compile-time power of two in [16, 4096]:
 // radix-16 passes, then one radix-2/4/8 pass for the remaining factor. The
 // first pass reads `src` (padded or not); later passes work in place on `buf`.
-template <int M, bool INV, bool SRC_PADDED, int NS = 1, typename V>
-__device__ __forceinline__ void cfft(const V* src, V* buf, const V* __restrict__ tw, int tws) {
+template <int M, bool INV, bool SRC_PADDED, int NS = 1, typename V, typename TW>
+__device__ __forceinline__ void cfft(const V* src, V* buf, const TW& tw) {
     constexpr int REM = M / NS;
     if constexpr (REM >= 16) {
-        stockham_pass<16, INV, SRC_PADDED>(src, buf, M, NS, tw, tws);
-        cfft<M, INV, true, NS * 16>(buf, buf, tw, tws);
+        stockham_pass<16, INV, SRC_PADDED>(src, buf, M, NS, tw);
+        cfft<M, INV, true, NS * 16>(buf, buf, tw);
     } else if constexpr (REM > 1) {
-        stockham_pass<REM, INV, SRC_PADDED>(src, buf, M, NS, tw, tws);
+        stockham_pass<REM, INV, SRC_PADDED>(src, buf, M, NS, tw);
     }
 }
 
@@ -215,9 +243,9 @@ __device__ __forceinline__ void cfft(const V* src, V* buf, const V* __restrict__
 //   forward:  X[k] = E[k] + W_N^k O[k],  E = (Z_k + Z*_{M-k})/2, O = (Z_k - Z*_{M-k})/(2i)
 //   op:       Y[k] = op(X[k], k)         (must keep Y Hermitian-consistent)
 //   inverse:  Z'[k] = E' + i O',  E' = (Y_k + Y*_{M-k})/2, O' = (Y_k - Y*_{M-k}) conj(W_N^k)/2
-// twN = e^{-2 pi i k / N} for k in [0, M].
-template <typename V, typename Op>
-__device__ __forceinline__ void real_spectral_op(V* buf, int M, const V* __restrict__ twN, Op op) {
+// tw.h(k) = e^{-2 pi i k / N} for k in [0, M].
+template <typename V, typename TW, typename Op>
+__device__ __forceinline__ void real_spectral_op(V* buf, int M, const TW& tw, Op op) {
     using R = decltype(V{}.x);
     for (int k = gtid(); k <= M / 2; k += kGroupThreads) {
         if (k == 0) {
@@ -234,7 +262,7 @@ __device__ __forceinline__ void real_spectral_op(V* buf, int M, const V* __restr
         }
         const int kk = M - k;
         const V zk = buf[pad16(k)], zkk = buf[pad16(kk)];
-        const V wk = twN[k], wkk = twN[kk];
+        const V wk = tw.h(k), wkk = tw.h(kk);
         // forward split
         const V ek = {(R)0.5 * (zk.x + zkk.x), (R)0.5 * (zk.y - zkk.y)};
         const V dk = {(R)0.5 * (zk.x - zkk.x), (R)0.5 * (zk.y + zkk.y)}; // (Z_k - Z*_kk)/2

@@ -159,13 +159,13 @@ __global__ void __launch_bounds__(kThreads) k_matched_filter(MfArgs a) {
     const double* x = a.mf + row * a.mf_len;
     for (int i = threadIdx.x; i < N; i += blockDim.x) bufA[i] = i < a.mf_len ? x[i] : 0.0;
     __syncthreads();
-    cfft<M, false, false>(reinterpret_cast<const double2*>(bufA), bufB, a.tw, 2);
+    cfft<M, false, false>(reinterpret_cast<const double2*>(bufA), bufB, TwGlobal<double2>{a.tw, 2});
     const double scale = 2.0 / (double)N;
     const double2* R = a.ref_spec;
-    real_spectral_op(bufB, M, a.tw, [&](double2 X, int k) {
+    real_spectral_op(bufB, M, TwGlobal<double2>{a.tw, 2}, [&](double2 X, int k) {
         return cmul(X, double2{R[k].x * scale, R[k].y * scale});
     });
-    cfft<M, true, true>(bufB, bufB, a.tw, 2);
+    cfft<M, true, true>(bufB, bufB, TwGlobal<double2>{a.tw, 2});
     // padded rows: sample n at [row * Lp + H + n]; the halo stays zero
     double* out = a.filt + row * a.Lp + a.H;
     float* out32 = a.filt32 ? a.filt32 + row * a.Lp + a.H : nullptr;
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kThreads) k_rfft_forward(const double* x, doub
     double2* bufB = reinterpret_cast<double2*>(bufA + N);
     for (int i = threadIdx.x; i < N; i += blockDim.x) bufA[i] = x[i];
     __syncthreads();
-    cfft<M, false, false>(reinterpret_cast<const double2*>(bufA), bufB, tw, 2);
+    cfft<M, false, false>(reinterpret_cast<const double2*>(bufA), bufB, TwGlobal<double2>{tw, 2});
     for (int k = threadIdx.x; k <= M; k += blockDim.x) {
         const int k1 = k % M, k2 = (M - k) % M;
         const double2 zk = bufB[pad16(k1)], zkk = bufB[pad16(k2)];
@@ -377,14 +377,24 @@ __global__ void __launch_bounds__(kThreads * G, SNB_ENV_MINB / G) k_envelope(Env
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int N = 2 * M;
     const int grp = gidx(), tid = gtid();
-    R* comp = reinterpret_cast<R*>(smem);
-    const int comp_pad = (a.fir_q * a.decim + 1) & ~1;
+    constexpr bool kSmemTw = M == kTwSharedM;
+    V* tws = reinterpret_cast<V*>(smem);                   // compact twiddles (M == 4096)
+    R* comp = reinterpret_cast<R*>(tws + (kSmemTw ? kTwSharedCount : 0));
+    const int comp_pad = a.fir_fast ? 0 : (a.fir_q * a.decim + 1) & ~1;
     const int group_reals = envelope_group_reals(N, a.decim * a.phase_len);
     V* bufB = reinterpret_cast<V*>(comp + comp_pad + (size_t)grp * group_reals);
     const R* cr = reinterpret_cast<const R*>(a.comp);
     const V* tw = reinterpret_cast<const V*>(a.tw);
     for (int i = threadIdx.x; i < comp_pad; i += blockDim.x) comp[i] = i < a.comp_len ? cr[i] : (R)0;
+    if constexpr (kSmemTw) {
+        const V* src = reinterpret_cast<const V*>(a.tw_small);
+        for (int i = threadIdx.x; i < kTwSharedCount; i += blockDim.x) tws[i] = src[i];
+    }
     __syncthreads();
+    using TWT = typename std::conditional<kSmemTw, TwShared<V>, TwGlobal<V>>::type;
+    TWT twsrc;
+    if constexpr (kSmemTw) twsrc = TwShared<V>{tws};
+    else twsrc = TwGlobal<V>{tw, 2};
     const int64_t L = a.mf_len;
     const int64_t items = a.n_dirs * a.batch;
     const R scale = (R)2 / (R)N;
@@ -393,12 +403,12 @@ __global__ void __launch_bounds__(kThreads * G, SNB_ENV_MINB / G) k_envelope(Env
     for (int64_t it = (int64_t)blockIdx.x * G + grp; it < items; it += (int64_t)gridDim.x * G) {
         const int64_t b = it / a.n_dirs, slot = it % a.n_dirs;
         const R* src = reinterpret_cast<const R*>(a.beams) + (size_t)it * N;
-        cfft<M, false, false>(reinterpret_cast<const V*>(src), bufB, tw, 2);
-        real_spectral_op(bufB, M, tw, [&](V X, int k) {
+        cfft<M, false, false>(reinterpret_cast<const V*>(src), bufB, twsrc);
+        real_spectral_op(bufB, M, twsrc, [&](V X, int k) {
             if (k == 0 || k == M) return V{(R)0, (R)0};
             return V{X.y * scale, -X.x * scale}; // -i X, with the 2/N of the inverse
         });
-        cfft<M, true, true>(bufB, bufB, tw, 2);
+        cfft<M, true, true>(bufB, bufB, twsrc);
         // |b + iH(b)|: h from the inverse FFT (shared), b re-read from the beam
         // buffer; values kept in registers across the barrier, then written in
         // the decimation-phase layout e_p[u] = env[u*D - c0 + p] (zero outside
@@ -578,7 +588,8 @@ void launch_beamform_tiles(const BeamArgs& a, bool f32, cudaStream_t s) {
 
 size_t envelope_smem_bytes(int n, int comp_taps_padded, int phase_reals, bool f32, int groups) {
     const size_t rb = f32 ? 4 : 8;
-    return (size_t)((comp_taps_padded + 1) & ~1) * rb +
+    return (n / 2 == kTwSharedM ? (size_t)kTwSharedCount * 2 * rb : 0) +
+           (size_t)((comp_taps_padded + 1) & ~1) * rb +
            (size_t)groups * envelope_group_reals(n, phase_reals) * rb;
 }
 

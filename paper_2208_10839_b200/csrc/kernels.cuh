@@ -67,6 +67,7 @@ struct EnvArgs {
     const int32_t* order;    // slot -> direction
     const void* comp;        // composite reversed kernel (f64 or f32)
     const void* tw;          // twiddles for N (double2 or float2)
+    const void* tw_small;    // TwShared tables (fft.cuh), used when N == 8192
     int64_t mf_len, bins, n_dirs;
     int n, comp_len, decim, batch;
     int fir_q;               // ceil(comp_len / decim): taps per phase

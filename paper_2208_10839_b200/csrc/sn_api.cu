@@ -4,6 +4,7 @@
 // (pipeline.cpp:191-319): everything is derived and allocated at creation
 // (device tables, per-stage buffers for max_batch measurements, pinned
 // staging, one CUDA stream); process calls only enqueue kernels and copies.
+#include "fft.cuh"
 #include "kernels.cuh"
 #include "plan.hpp"
 #include "sonarnet_b200.h"
@@ -83,6 +84,28 @@ std::vector<double2> twiddles(uint64_t n) {
     return tw;
 }
 
+// Compact twiddle set of TwShared (fft.cuh) for M = 4096 (N = 8192): per-pass
+// tables e^{-2 pi i step e / M} for the radix-16 passes at ns = 16 and 256
+// (e = 1, 2, 4, 8) and the two-level split/merge table A[a] = e^{-2 pi i 64a/N},
+// B[b] = e^{-2 pi i b/N}.
+std::vector<double2> twiddles_small() {
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    auto e = [&](long double num, long double den) {
+        const long double a = two_pi * num / den;
+        return double2{(double)cosl(a), (double)-sinl(a)};
+    };
+    std::vector<double2> t;
+    const int M = kTwSharedM, N = 2 * kTwSharedM;
+    for (int ns : {16, 256}) {
+        for (int k = 0; k < ns; ++k) {
+            for (int ex : {1, 2, 4, 8}) t.push_back(e((long double)(M / (ns * 16)) * k * ex, M));
+        }
+    }
+    for (int a = 0; a <= 64; ++a) t.push_back(e(64.0L * a, N));
+    for (int b = 0; b < 64; ++b) t.push_back(e(b, N));
+    return t;
+}
+
 } // namespace
 
 struct sn_workspace {
@@ -116,6 +139,8 @@ struct sn_workspace {
     double2* d_tw_mf = nullptr;
     double2* d_tw_env = nullptr;
     float2* d_tw_env32 = nullptr;
+    double2* d_tw_small = nullptr;
+    float2* d_tw_small32 = nullptr;
     uint8_t* h_in = nullptr;
     float* h_out = nullptr;
     // launch shapes
@@ -154,7 +179,7 @@ struct sn_workspace {
         for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
                         (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot,  (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
-                        (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32}) {
+                        (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32, (void*)d_tw_small, (void*)d_tw_small32}) {
             if (p) cudaFree(p);
         }
         if (h_in) cudaFreeHost(h_in);
@@ -235,6 +260,15 @@ struct sn_workspace {
         std::vector<float2> tw32(s.env_fft);
         for (uint64_t k = 0; k < s.env_fft; ++k) tw32[k] = float2{(float)tw_env[k].x, (float)tw_env[k].y};
         upload(d_tw_env32, tw32, stream);
+        {
+            const auto ts = twiddles_small();
+            d_tw_small = dmalloc<double2>(ts.size(), n);
+            d_tw_small32 = dmalloc<float2>(ts.size(), n);
+            upload(d_tw_small, ts, stream);
+            std::vector<float2> ts32(ts.size());
+            for (size_t k = 0; k < ts.size(); ++k) ts32[k] = float2{(float)ts[k].x, (float)ts[k].y};
+            upload(d_tw_small32, ts32, stream);
+        }
         // reference spectrum: rfft of the reversed chirp zero-padded to mf_fft
         // (pipeline.cpp:274-278)
         {
@@ -346,6 +380,7 @@ struct sn_workspace {
         ea.order = d_order;
         ea.comp = f32 ? (const void*)d_comp32 : (const void*)d_comp;
         ea.tw = f32 ? (const void*)d_tw_env32 : (const void*)d_tw_env;
+        ea.tw_small = f32 ? (const void*)d_tw_small32 : (const void*)d_tw_small;
         ea.mf_len = (int64_t)z.mf_len;
         ea.bins = (int64_t)z.bins;
         ea.n_dirs = (int64_t)z.n_dirs;
