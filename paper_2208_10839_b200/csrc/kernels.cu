@@ -169,12 +169,22 @@ __global__ void __launch_bounds__(kThreads) k_matched_filter(MfArgs a) {
     // padded rows: sample n at [row * Lp + H + n]; the halo stays zero
     double* out = a.filt + row * a.Lp + a.H;
     float* out32 = a.filt32 ? a.filt32 + row * a.Lp + a.H : nullptr;
+    double amax = 0.0;
     for (int64_t n = threadIdx.x; n < a.mf_len; n += blockDim.x) {
         const int64_t q = n + a.ref_len - 1;
         const double2 z = bufB[pad16((int)(q >> 1))];
         const double v = (q & 1) ? z.y : z.x;
         out[n] = v;
+        amax = fmax(amax, fabs(v));
         if (out32) out32[n] = (float)v;
+    }
+    if (a.amax_bits) {
+        // per-capture max |filt| (block-floating-point scale of the tensor-core
+        // beamformer); non-negative doubles order like their bit patterns
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        if ((threadIdx.x & 31) == 0)
+            atomicMax(a.amax_bits + blockIdx.y, (unsigned long long)__double_as_longlong(amax));
     }
 }
 

@@ -51,6 +51,7 @@ struct MfArgs {
     const double2* tw;      // e^{-2 pi i k/N}, k < N
     int64_t mf_len, Lp;
     int n, ref_len, H;
+    unsigned long long* amax_bits; // optional [B] max |filt| (as double bits), zeroed by the caller
 };
 
 struct BeamArgs {
@@ -104,6 +105,34 @@ void launch_beamform(const double* filt, double* beams, const int32_t* shifts, i
                      int64_t n_dirs, cudaStream_t s);
 
 double measure_fma_peak(int sms, bool f32);
+
+// ---- tensor-core delay-and-sum (beamform_tc.cu) ---------------------------
+constexpr int kTcM = 128;      // directions per cluster (MMA M)
+constexpr int kTcN = 80;       // time samples per tile (MMA N); 6 x 80 TMEM columns
+constexpr int kTcSlices = 6;   // balanced base-256 digits of the 46-bit fixed-point samples
+constexpr int kTcRChunk = 8;   // shift values per A-operand chunk (double-buffered)
+struct DigitArgs {
+    const double* filt;                // [B][32][Lp], sample n at H + n
+    const unsigned long long* amax_bits; // [B]
+    const int32_t* base;               // [C][32] per-cluster channel base shift
+    int8_t* planes;                    // [B][C][6][2][rows][16]
+    int64_t L, Lp;
+    int H, rows, pad, clusters;
+};
+struct TcArgs {
+    const int8_t* planes;              // as DigitArgs
+    const uint8_t* resid;              // [C * 128][32] shift - base (0xFF: unused row)
+    const int32_t* R;                  // [C] shift values per cluster
+    const unsigned long long* amax_bits;
+    void* beams;                       // [B][n_dirs][N] slot order, f64 or f32
+    int64_t L, N, n_dirs;
+    int rows, pad, clusters, ntiles, batch, f32;
+};
+constexpr int kTcMaxGrid = 512;
+struct TcSched { int start[kTcMaxGrid + 1]; }; // CTA k processes tiles [start[k], start[k+1])
+void launch_digits(const DigitArgs& a, int batch, cudaStream_t s);
+void launch_beamform_tc(const TcArgs& a, const TcSched& sched, int grid, cudaStream_t s);
+size_t beamform_tc_smem_bytes(int rmax);
 
 size_t demod_smem_bytes(int octets, int words);
 size_t fft_smem_bytes(int n, int real_bytes);

@@ -10,6 +10,7 @@
 #include "sonarnet_b200.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -148,6 +149,15 @@ struct sn_workspace {
     int demod_grid = 0;
     size_t demod_smem = 0, mf_smem = 0, dir_smem = 0;
     int dir_grid = 0, halo = 0, tile = 0, fir_q = 0, phase_len = 0, fir_fast = 0;
+    // tensor-core beamformer (beamform_tc.cu)
+    bool tc = false;
+    int tc_clusters = 0, tc_pad = 0, tc_rows = 0, tc_ntiles = 0, tc_grid = 0;
+    std::vector<int32_t> tc_R;
+    int8_t* d_planes = nullptr;
+    uint8_t* d_resid = nullptr;
+    int32_t* d_tc_R = nullptr;
+    int32_t* d_tc_base = nullptr;
+    unsigned long long* d_amax = nullptr;
     FirTaps<double> taps64{};
     FirTaps<float> taps32{};
     uint64_t packed_bytes = 0, energy_per = 0, lp = 0;
@@ -179,7 +189,8 @@ struct sn_workspace {
         for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
                         (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot,  (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
-                        (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32, (void*)d_tw_small, (void*)d_tw_small32}) {
+                        (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32, (void*)d_tw_small, (void*)d_tw_small32, (void*)d_planes, (void*)d_resid,
+                        (void*)d_tc_R, (void*)d_tc_base, (void*)d_amax}) {
             if (p) cudaFree(p);
         }
         if (h_in) cudaFreeHost(h_in);
@@ -312,6 +323,7 @@ struct sn_workspace {
         demod_grid = std::max(1, sms * per_sm / P);
         // beamformer time tile: 32 x (T + 2H) samples staged per CTA
         tile = 128;
+        init_tensor_core_beamformer(sms);
         {
             // polyphase FIR rows (fir_polyphase in kernels.cu): every envelope
             // sample needs a slot and every FIR read stays inside its row
@@ -343,6 +355,76 @@ struct sn_workspace {
         ck(cudaStreamSynchronize(stream), "setup sync");
     }
 
+    // Tensor-core delay-and-sum setup: clusters of kTcM consecutive slots, the
+    // per-cluster channel base shift b_i (min over the cluster), the residual
+    // bytes s - b_i per slot and the shift count R_c (beamform_tc.cu).
+    // SNB_BEAMFORMER=tiles selects the CUDA-core tiled kernel instead.
+    void init_tensor_core_beamformer(int sms) {
+        const char* env = std::getenv("SNB_BEAMFORMER");
+        tc = !(env && std::string(env) == "tiles");
+        if (!tc) return;
+        const Sizes& s = plan.sz;
+        const uint64_t nd = s.n_dirs;
+        tc_clusters = (int)((nd + kTcM - 1) / kTcM);
+        std::vector<int32_t> base((size_t)tc_clusters * kCh, 0);
+        std::vector<uint8_t> resid((size_t)tc_clusters * kTcM * kCh, 0xFF);
+        tc_R.assign(tc_clusters, 1);
+        for (int c = 0; c < tc_clusters; ++c) {
+            const uint64_t s0 = (uint64_t)c * kTcM, s1 = std::min<uint64_t>(nd, s0 + kTcM);
+            int R = 1;
+            for (int i = 0; i < kCh; ++i) {
+                int lo = 1 << 30, hi = -(1 << 30);
+                for (uint64_t sl = s0; sl < s1; ++sl) {
+                    lo = std::min(lo, plan.shifts[sl * kCh + i]);
+                    hi = std::max(hi, plan.shifts[sl * kCh + i]);
+                }
+                base[(size_t)c * kCh + i] = lo;
+                R = std::max(R, hi - lo + 1);
+                for (uint64_t sl = s0; sl < s1; ++sl) resid[sl * kCh + i] = (uint8_t)(plan.shifts[sl * kCh + i] - lo);
+            }
+            if (R > 250) { tc = false; return; }
+            tc_R[c] = R;
+        }
+        const int rmax = *std::max_element(tc_R.begin(), tc_R.end());
+        tc_pad = (rmax + 6) & ~7; // >= rmax - 1, multiple of 8
+        tc_ntiles = (int)((s.mf_len + kTcN - 1) / kTcN);
+        tc_rows = tc_pad + tc_ntiles * kTcN;
+        uint64_t& n = device_allocs;
+        d_planes = dmalloc<int8_t>(max_batch * (uint64_t)tc_clusters * 12 * tc_rows * 16, n);
+        d_resid = dmalloc<uint8_t>(resid.size(), n);
+        d_tc_R = dmalloc<int32_t>(tc_R.size(), n);
+        d_tc_base = dmalloc<int32_t>(base.size(), n);
+        d_amax = dmalloc<unsigned long long>(max_batch, n);
+        upload(d_resid, resid, stream);
+        upload(d_tc_R, tc_R, stream);
+        upload(d_tc_base, base, stream);
+        tc_grid = std::min(sms, kTcMaxGrid);
+    }
+
+    // contiguous per-CTA tile ranges of equal estimated work (R_c + 8 units
+    // per tile: MMAs plus window load and epilogue)
+    TcSched tc_schedule(int count) const {
+        TcSched sc{};
+        const int per_c = count * tc_ntiles;
+        double total = 0;
+        for (int c = 0; c < tc_clusters; ++c) total += (double)(tc_R[c] + 8) * per_c;
+        int k = 1;
+        double acc = 0;
+        sc.start[0] = 0;
+        for (int c = 0; c < tc_clusters && k < tc_grid; ++c) {
+            const double w = tc_R[c] + 8;
+            while (k < tc_grid && acc + w * per_c >= total * k / tc_grid) {
+                const double need = total * k / tc_grid - acc;
+                int m = (int)std::ceil(need / w);
+                m = std::max(0, std::min(per_c, m));
+                sc.start[k++] = c * per_c + m;
+            }
+            acc += w * per_c;
+        }
+        for (; k <= tc_grid; ++k) sc.start[k] = tc_clusters * per_c;
+        return sc;
+    }
+
     // Enqueue the whole pipeline for `count` measurements (count <= max_batch).
     void enqueue(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s) {
         const Sizes& z = plan.sz;
@@ -357,10 +439,32 @@ struct sn_workspace {
                      (int)plan.premf_rev.size(), plan.cfg.pre_mf_decimation};
         launch_premf(pa, (int)count, s);
         if (profiling) cudaEventRecord(ev[2], s);
-        MfArgs ma{d_mf, d_filt, f32 ? d_filt32 : nullptr, d_ref_spec, d_tw_mf,
-                  (int64_t)z.mf_len, (int64_t)lp, (int)z.mf_fft, (int)z.ref_len, halo};
+        MfArgs ma{d_mf, d_filt, f32 && !tc ? d_filt32 : nullptr, d_ref_spec, d_tw_mf,
+                  (int64_t)z.mf_len, (int64_t)lp, (int)z.mf_fft, (int)z.ref_len, halo, tc ? d_amax : nullptr};
+        if (tc) ck(cudaMemsetAsync(d_amax, 0, count * sizeof(unsigned long long), s), "memset");
         launch_matched_filter(ma, (int)count, mf_smem, s);
         if (profiling) cudaEventRecord(ev[3], s);
+        if (tc) {
+            DigitArgs dg{d_filt, d_amax, d_tc_base, d_planes, (int64_t)z.mf_len, (int64_t)lp, halo, tc_rows,
+                         tc_pad, tc_clusters};
+            launch_digits(dg, (int)count, s);
+            TcArgs ta{};
+            ta.planes = d_planes;
+            ta.resid = d_resid;
+            ta.R = d_tc_R;
+            ta.amax_bits = d_amax;
+            ta.beams = d_beams;
+            ta.L = (int64_t)z.mf_len;
+            ta.N = (int64_t)z.env_fft;
+            ta.n_dirs = (int64_t)z.n_dirs;
+            ta.rows = tc_rows;
+            ta.pad = tc_pad;
+            ta.clusters = tc_clusters;
+            ta.ntiles = tc_ntiles;
+            ta.batch = (int)count;
+            ta.f32 = f32 ? 1 : 0;
+            launch_beamform_tc(ta, tc_schedule((int)count), tc_grid, s);
+        } else {
         BeamArgs ba{};
         ba.filt = f32 ? (const void*)d_filt32 : (const void*)d_filt;
         ba.beams = d_beams;
@@ -373,6 +477,7 @@ struct sn_workspace {
         ba.T = tile;
         ba.batch = (int)count;
         launch_beamform_tiles(ba, f32, s);
+        }
         if (profiling) cudaEventRecord(ev[4], s);
         EnvArgs ea{};
         ea.beams = d_beams;
@@ -394,7 +499,7 @@ struct sn_workspace {
         launch_envelope(ea, taps32, taps64, f32, dir_grid, s);
         if (profiling) cudaEventRecord(ev[5], s);
         ck(cudaGetLastError(), "kernel launch");
-        last_launches = 5;
+        last_launches = tc ? 6 : 5;
     }
 
     void validate(const sn_raw_measurement& m) const { // pipeline.cpp:524-540
@@ -631,7 +736,7 @@ sn_status sn_workspace_process_device_graph(sn_workspace* ws, const uint8_t* d_p
             ws->g_count = count;
         }
         ck(cudaGraphLaunch(ws->graph, s), "graph launch");
-        ws->last_launches = 5;
+        ws->last_launches = ws->tc ? 6 : 5;
     });
 }
 
