@@ -3,9 +3,10 @@
 //
 // The reference (beamform_into, pipeline.cpp:432-446) forms, per direction d,
 //     y_d[n] = (1/32) sum_i x_i[n - s_{d,i}]          (zero outside [0, L))
-// with integer shifts s_{d,i} = delay - advance. For a cluster of 128
-// directions (consecutive k-d slots, Plan::order) the shifts of channel i lie
-// in [b_i, b_i + R) with R ~ 23 on the hemisphere3000 grid, so with the
+// with integer shifts s_{d,i} = delay - advance. For a cluster of <= 128
+// directions (consecutive k-d slots, Plan::order, cut so that R <= kTcRMax)
+// the shifts of channel i lie in [b_i, b_i + R) with R ~ 23 on the
+// hemisphere3000 grid, so with the
 // re-centred channels x'_i[t] = x_i[t - b_i]
 //     y_d[n] = sum_{r < R} sum_{i < 32} A_r[d][i] * x'_i[n - r],
 //     A_r[d][i] = (s_{d,i} - b_i == r)  in {0, 1}
@@ -13,14 +14,15 @@
 // dense steering-matrix contraction (the "0/1 steering matrix" of the
 // north star) whose B operand for shift r is the same time window displaced
 // by r rows. The samples are quantised to 46-bit block floating point per
-// capture (X = round(x * 2^46 / max|x|)), split into six balanced base-256
+// capture (X = round(x * 2^(46 - k)), 2^k > max|x|), split into six balanced base-256
 // digits (int8), and each digit plane is contracted separately with int32
 // accumulation in tensor memory (|sum| <= 32 * 128: exact). The epilogue
-// recombines Y = sum_j 256^j Y_j exactly in int64 and scales once:
-//     beam = fl(Y * max|x| * 2^-46 / 32)
-// — the exactly rounded sum of the quantised samples, whose error
-// (<= 2^-47 max|x|) is the same size as the reference's own FP64 summation
-// error (32 roundings of 2^-53 |partial|).
+// recombines Y = sum_j 256^j Y_j exactly in int64 and rescales by an exponent
+// add (integer instructions only):
+//     beam = Y * 2^(k - 46) / 32            (exact: |Y| < 2^53)
+// — the exact sum of the quantised samples, whose error (<= 2^-47 2^k, i.e.
+// <= 2^-46 max|x|) is the size of the reference's own FP64 summation error
+// (32 roundings of 2^-53 |partial|).
 //
 // Shared-memory operand layouts (SWIZZLE_NONE, K-major, 16-byte core rows):
 //   B window, per digit j and channel half h: rows q = 0 .. N + R - 2 of 16
@@ -28,14 +30,14 @@
 //     8 rows), the halves LBO apart. The operand for shift r starts at row
 //     R - 1 - r: any r is a 16-byte aligned descriptor offset, so the shifted
 //     operands are free (no copies).
-//   A_r: [half][128 rows][16 B], LBO = 2048 B, SBO = 128 B; built by the
-//     threads from their direction's residual bytes with one SIMD compare per
-//     4 channels, double-buffered in chunks of kTcRChunk shifts whose reuse is
-//     gated by tcgen05.commit -> mbarrier.
-// TMEM: 6 accumulators of N = 80 int32 columns (480 of 512), lane = direction.
+//   A_r: [half][128 rows][16 B], LBO = 2048 B, SBO = 128 B; all r < R of the
+//     current cluster resident (R * 4 KB), built once per cluster.
+// TMEM: two sets of 6 accumulators of N = 32 int32 columns (384 of 512),
+// lane = direction; MMA completion is tracked with tcgen05.commit -> mbarrier.
 #include "kernels.cuh"
 
 #include <cstdint>
+#include <cstdio>
 
 namespace snb {
 
@@ -96,11 +98,56 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         : "memory");
 }
 
+__device__ __forceinline__ uint32_t elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n}\n" : "=r"(pred));
+    return pred;
+}
+
+// Y * 2^e (|Y| < 2^53, exact) assembled with integer instructions only: the
+// FP64 pipe is busy (math-throttled) while the tensor core runs, the integer
+// ALUs are not.
+__device__ __forceinline__ double i64_ldexp_exact(long long Y, int e) {
+    const unsigned long long m = (unsigned long long)(Y < 0 ? -Y : Y);
+    const int lz = __clzll(m | 1ull);
+    const unsigned long long mant = (m << (lz + 1)) >> 12;
+    const unsigned long long bits = ((unsigned long long)(Y < 0) << 63) |
+                                    ((unsigned long long)(63 - lz + e + 1023) << 52) | mant;
+    return m ? __longlong_as_double((long long)bits) : 0.0;
+}
+
+// block-floating-point exponent of a capture: max|x| < 2^k
+__device__ __forceinline__ int bfp_exponent(unsigned long long amax_bits) {
+    const int ef = (int)((amax_bits >> 52) & 0x7FF);
+    return ef ? ef - 1022 : 0;
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+        "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
+
+template <int NCOL>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&v)[NCOL]) {
+    if constexpr (NCOL == 32) tmem_ld32(taddr, v);
+    else tmem_ld16(taddr, v);
+}
+
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(smem_dst)), "l"(gsrc) : "memory");
 }
 
-constexpr int kTcThreads = 128;
+constexpr int kSlots = 512 / kTcN;            // TMEM ring of accumulator slots of kTcN columns
+constexpr int kWin = 3;                       // B window buffers (loads run kWin - 1 tiles ahead)
+constexpr int kEpiWarps = 16;                  // epilogue warps; warp 8 produces and issues
+constexpr int kTcThreads = 32 * (kEpiWarps + 1);
 constexpr int kTmemCols = 512;
 constexpr int kABytes = 2 * kTcM * 16; // one shift: two channel halves x 128 rows x 16 B
 
@@ -117,8 +164,10 @@ __global__ void __launch_bounds__(128) k_digits(DigitArgs a) {
     const int h = blockIdx.x / nblk;
     const int row = (blockIdx.x % nblk) * 128 + threadIdx.x;
     if (row >= a.rows) return;
-    double amax = __longlong_as_double((long long)a.amax_bits[b]);
-    const double inv = amax > 0.0 ? 70368744177664.0 / amax : 0.0; // 2^46 / max|x|
+    // power-of-two scale 2^(46 - k), max|x| < 2^k: exact, and the epilogue
+    // rescales by an exponent add
+    const int kexp = bfp_exponent(a.amax_bits[b]);
+    const double inv = __longlong_as_double((long long)(46 - kexp + 1023) << 52);
     const int64_t t = (int64_t)row - a.pad;
     const double* fb = a.filt + ((size_t)b * 32 + 16 * h) * a.Lp + a.H;
     const int32_t* base = a.base + (size_t)c * 32 + 16 * h;
@@ -146,19 +195,46 @@ __global__ void __launch_bounds__(128) k_digits(DigitArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_beamform_tc: persistent, one CTA (4 warps) per SM; the work list of
-// (cluster, capture, time tile) is cut into contiguous per-CTA ranges of
-// equal estimated work (TcSched).
+// k_beamform_tc: persistent, one CTA per SM, warp-specialised:
+//   warp 8 (producer/issuer): builds the resident A_r of each cluster, fetches
+//     the B window of tile k+2 with bulk async copies (cp.async.bulk, completion
+//     on an mbarrier with a byte count) while the tensor core runs tile k, and
+//     issues the R x 6 MMAs of each tile (one elected lane);
+//   warps 0-7 (epilogue): warp w drains TMEM lane quarter w & 3, column half
+//     w >> 2 of the finished accumulator set, hands the set back (mbarrier),
+//     recombines the digits exactly with integer instructions and stores FP64.
+// Handshakes: wfull[3] (window landed), wfree[3] (MMAs that read a window are
+// done, tcgen05.commit), afull[2] (accumulator set complete, tcgen05.commit),
+// aempty[2] (8 epilogue warps drained the set). The work list of
+// (cluster, capture, time tile) is cut into contiguous per-CTA ranges of equal
+// estimated work (TcSched); tile g of a CTA uses window g % 3 and TMEM set g & 1.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(bar))
+                 : "memory");
+}
+
 __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const __grid_constant__ TcSched sched) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int wrows = kTcN + a.pad;                 // window rows per (digit, half)
-    uint8_t* Bw = smem;                             // [12][wrows][16]
-    uint8_t* Ab = Bw + (size_t)12 * wrows * 16;     // [2][kTcRChunk][kABytes]
-    Ab = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(Ab) + 127) & ~uintptr_t(127));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(Ab + 2 * kTcRChunk * kABytes); // chunk 0, chunk 1, acc
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wrows = kTcN + a.pad;                     // window rows per (digit, half)
+    const size_t bbuf = (size_t)12 * wrows * 16;        // one B window set
+    uint8_t* Ares = smem;                               // [rmax][2][128][16]
+    uint8_t* Bw = smem + (size_t)a.rmax * kABytes;      // [kWin][12][wrows][16]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Bw + kWin * bbuf);
+    uint64_t* wfull = bars;           // [kWin]
+    uint64_t* wfree = bars + kWin;    // [kWin]
+    uint64_t* sfull = bars + 2 * kWin;  // [kSlots]
+    uint64_t* sempty = sfull + kSlots;  // [kSlots]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + kSlots);
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
                      "n"(kTmemCols)
@@ -166,136 +242,169 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        mbar_init(&bars[2], 1);
+        for (int i = 0; i < kWin; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wfree[i], 1); }
+        for (int i = 0; i < kSlots; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], kEpiWarps); }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    const uint32_t idesc = idesc_i8(kTcM, kTcN);
-    const uint32_t bw_addr = su32(Bw), ab_addr = su32(Ab);
-    uint32_t ph0 = 0, ph1 = 0, ph_acc = 0;
-    bool pend0 = false, pend1 = false;
     const int per_cb = a.batch * a.ntiles;
-    for (int t = sched.start[blockIdx.x]; t < sched.start[blockIdx.x + 1]; ++t) {
-        const int c = t / per_cb, rem = t - c * per_cb;
-        const int b = rem / a.ntiles, tt = rem - b * a.ntiles;
-        const int64_t t0 = (int64_t)tt * kTcN;
-        const int R = a.R[c];
-        // ---- B window: 12 planes x (N + R - 1) rows, async copies
-        {
-            const int nq = kTcN + R - 1;
-            const int8_t* pb = a.planes + (((size_t)b * a.clusters + c) * 12 * a.rows + (a.pad + t0 - (R - 1))) * 16;
-            for (int idx = tid; idx < 12 * nq; idx += kTcThreads) {
-                const int jh = idx / nq, q = idx - jh * nq;
-                cp_async16(Bw + ((size_t)jh * wrows + q) * 16, pb + ((size_t)jh * a.rows + q) * 16);
+    const int t_beg = sched.start[blockIdx.x], t_end = sched.start[blockIdx.x + 1];
+    const int ntile = t_end - t_beg;
+
+    if (warp == kEpiWarps) {
+        // ===================== producer / MMA issuer warp =====================
+        const uint32_t idesc = idesc_i8(kTcM, kTcN);
+        const uint32_t ares_addr = su32(Ares), bw_addr = su32(Bw);
+        const bool leader = elect_one();
+        auto load_window = [&](int g) {
+            const int t = t_beg + g;
+            const int c = t / per_cb, rem = t - c * per_cb;
+            const int b = rem / a.ntiles, tt = rem - b * a.ntiles;
+            const int R = a.R[c];
+            const uint32_t bytes = (uint32_t)(kTcN + R - 1) * 16;
+            const int8_t* pb = a.planes +
+                (((size_t)b * a.clusters + c) * 12 * a.rows + (size_t)(a.pad + tt * kTcN - (R - 1))) * 16;
+            uint8_t* dst = Bw + (size_t)(g % kWin) * bbuf;
+            if (leader) {
+                mbar_expect_tx(&wfull[g % kWin], 12 * bytes);
+                for (int jh = 0; jh < 12; ++jh)
+                    bulk_g2s(dst + (size_t)jh * wrows * 16, pb + (size_t)jh * a.rows * 16, bytes, &wfull[g % kWin]);
             }
-            asm volatile("cp.async.commit_group;\n" ::: "memory");
-        }
-        // my direction's residual bytes (0xFF on padding rows: never equal to r)
-        uint32_t res[8];
-        {
-            const uint4* rp = reinterpret_cast<const uint4*>(a.resid + ((size_t)c * kTcM + tid) * 32);
-            const uint4 r0 = rp[0], r1 = rp[1];
-            res[0] = r0.x; res[1] = r0.y; res[2] = r0.z; res[3] = r0.w;
-            res[4] = r1.x; res[5] = r1.y; res[6] = r1.z; res[7] = r1.w;
-        }
-        const int nchunks = (R + kTcRChunk - 1) / kTcRChunk;
-        for (int q = 0; q < nchunks; ++q) {
-            const int buf = q & 1;
-            if (buf == 0 && pend0) { mbar_wait(&bars[0], ph0); ph0 ^= 1; pend0 = false; }
-            if (buf == 1 && pend1) { mbar_wait(&bars[1], ph1); ph1 ^= 1; pend1 = false; }
-            uint8_t* abuf = Ab + (size_t)buf * kTcRChunk * kABytes;
+            __syncwarp();
+        };
+        auto build_A = [&](int c) {
+            const int R = a.R[c];
+            uint4* z = reinterpret_cast<uint4*>(Ares);
+            for (int i = lane; i < R * (kABytes / 16); i += 32) z[i] = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+            for (int d = lane; d < kTcM; d += 32) {
+                const uint4* rp = reinterpret_cast<const uint4*>(a.resid + ((size_t)c * kTcM + d) * 32);
 #pragma unroll
-            for (int rr = 0; rr < kTcRChunk; ++rr) {
-                const int r = q * kTcRChunk + rr;
-                if (r < R) {
-                    const uint32_t pat = 0x01010101u * (uint32_t)r;
+                for (int h = 0; h < 2; ++h) {
+                    const uint4 rw = rp[h];
+                    const uint32_t w[4] = {rw.x, rw.y, rw.z, rw.w};
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        uint4 v;
-                        v.x = __vcmpeq4(res[4 * h + 0], pat) & 0x01010101u;
-                        v.y = __vcmpeq4(res[4 * h + 1], pat) & 0x01010101u;
-                        v.z = __vcmpeq4(res[4 * h + 2], pat) & 0x01010101u;
-                        v.w = __vcmpeq4(res[4 * h + 3], pat) & 0x01010101u;
-                        *reinterpret_cast<uint4*>(abuf + (size_t)rr * kABytes + h * (kTcM * 16) + tid * 16) = v;
+                    for (int i = 0; i < 16; ++i) {
+                        const int r = (w[i >> 2] >> (8 * (i & 3))) & 0xFF; // 0xFF: padding row
+                        if (r < R) Ares[(size_t)r * kABytes + h * (kTcM * 16) + d * 16 + i] = 1;
                     }
                 }
             }
-            if (q == 0) asm volatile("cp.async.wait_all;\n" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            __syncthreads();
-            if (tid == 0) {
-                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                for (int rr = 0; rr < kTcRChunk; ++rr) {
-                    const int r = q * kTcRChunk + rr;
-                    if (r >= R) break;
-                    const uint64_t ad = sdesc(ab_addr + (uint32_t)((buf * kTcRChunk + rr) * kABytes), kTcM * 16, 128);
-#pragma unroll
-                    for (int j = 0; j < kTcSlices; ++j) {
-                        const uint32_t boff = (uint32_t)(((2 * j) * wrows + (R - 1 - r)) * 16);
-                        const uint64_t bd = sdesc(bw_addr + boff, (uint32_t)(wrows * 16), 128);
-                        mma_i8(tmem + (uint32_t)(j * kTcN), ad, bd, idesc, r > 0 ? 1u : 0u);
-                    }
-                }
-                mma_commit(&bars[buf]);
-                if (q == nchunks - 1) mma_commit(&bars[2]);
+            __syncwarp();
+        };
+        int cur_c = -1;
+        for (int g = 0; g < kWin - 1 && g < ntile; ++g) load_window(g);
+        for (int g = 0; g < ntile; ++g) {
+            const int t = t_beg + g;
+            const int c = t / per_cb;
+            const int R = a.R[c];
+            if (c != cur_c) {
+                // every MMA that read the old A has completed (commit of tile g - 1)
+                if (g > 0) mbar_wait(&wfree[(g - 1) % kWin], (uint32_t)(((g - 1) / kWin) & 1));
+                build_A(c);
+                cur_c = c;
             }
-            if (buf == 0) pend0 = true;
-            else pend1 = true;
-        }
-        // ---- epilogue: exact recombination of the six digit products
-        mbar_wait(&bars[2], ph_acc);
-        ph_acc ^= 1;
-        if (pend0) { mbar_wait(&bars[0], ph0); ph0 ^= 1; pend0 = false; }
-        if (pend1) { mbar_wait(&bars[1], ph1); ph1 ^= 1; pend1 = false; }
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const int64_t slot = (int64_t)c * kTcM + tid;
-        const double amax = __longlong_as_double((long long)a.amax_bits[b]);
-        const double scale = amax * (1.0 / 70368744177664.0) * (1.0 / 32.0);
-        const bool live = slot < a.n_dirs;
-        const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-        for (int cc = 0; cc < kTcN / 16; ++cc) {
-            uint32_t y[kTcSlices][16];
-#pragma unroll
-            for (int j = 0; j < kTcSlices; ++j) tmem_ld16(trow + (uint32_t)(j * kTcN + cc * 16), y[j]);
-            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-            if (live) {
-                const int64_t n0 = t0 + cc * 16;
-                double v[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    long long Y = 0;
-#pragma unroll
-                    for (int j = kTcSlices - 1; j >= 0; --j) Y = Y * 256 + (long long)(int32_t)y[j][i];
-                    v[i] = (double)Y * scale;
+            // window g + kWin - 1 reuses the buffer of tile g - 1
+            if (g + kWin - 1 < ntile) {
+                if (g >= 1) mbar_wait(&wfree[(g - 1) % kWin], (uint32_t)(((g - 1) / kWin) & 1));
+                load_window(g + kWin - 1);
+            }
+            mbar_wait(&wfull[g % kWin], (uint32_t)((g / kWin) & 1));
+            const uint32_t bbase = bw_addr + (uint32_t)((g % kWin) * bbuf);
+            const uint64_t a0 = sdesc(ares_addr, kTcM * 16, 128);
+            const uint64_t b0 = sdesc(bbase + (uint32_t)((R - 1) * 16), (uint32_t)(wrows * 16), 128);
+            // digit planes high to low (the epilogue folds Y = Y * 256 + Y_j),
+            // each into the next TMEM slot of the ring
+            for (int p = 0; p < kTcSlices; ++p) {
+                const int j = kTcSlices - 1 - p;
+                const int q = kTcSlices * g + p, sl = q % kSlots;
+                if (q >= kSlots) mbar_wait(&sempty[sl], (uint32_t)(((q - kSlots) / kSlots) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                if (leader) {
+                    uint64_t ad = a0;
+                    uint64_t bd = b0 + (uint64_t)(2 * wrows * j); // plane j, 16-byte units
+                    const uint32_t tacc = tmem + (uint32_t)(sl * kTcN);
+                    for (int r = 0; r < R; ++r) {
+                        mma_i8(tacc, ad, bd, idesc, r > 0 ? 1u : 0u);
+                        ad += (uint64_t)(kABytes >> 4);
+                        bd -= 1;
+                    }
+                    mma_commit(&sfull[sl]);
                 }
+                __syncwarp();
+            }
+            if (leader) mma_commit(&wfree[g % kWin]);
+            __syncwarp();
+        }
+    } else {
+        // ======================== epilogue warps 0-15 =========================
+        // warp w: TMEM lane quarter w & 3 (directions), column quarter w >> 2
+        const int quarter = warp & 3, colq = warp >> 2;
+        const int d = quarter * 32 + lane;
+        constexpr int NC = kTcN / 4; // columns per thread
+        static_assert(NC == 16 || NC == 32, "epilogue column chunk");
+        for (int g = 0; g < ntile; ++g) {
+            const int t = t_beg + g;
+            const int c = t / per_cb, rem = t - c * per_cb;
+            const int b = rem / a.ntiles, tt = rem - b * a.ntiles;
+            const bool live = d < __ldg(a.cl_size + c);
+            const int64_t slot = (int64_t)__ldg(a.cl_start + c) + d;
+            const int eadj = bfp_exponent(__ldg(a.amax_bits + b)) - 46 - 5; // beam = Y 2^(k - 46) / 32
+            int32_t yh[NC], yl[NC];
+#pragma unroll
+            for (int p = 0; p < kTcSlices; ++p) {
+                const int q = kTcSlices * g + p, sl = q % kSlots;
+                mbar_wait(&sfull[sl], (uint32_t)((q / kSlots) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                uint32_t y[NC];
+                tmem_ld_cols<NC>(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sl * kTcN + colq * NC), y);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sempty[sl]);
+                // planes 5, 4, 3 -> Y_hi; 2, 1, 0 -> Y_lo (|.| < 2^29, exact in int32)
+#pragma unroll
+                for (int i = 0; i < NC; ++i) {
+                    if (p == 0) yh[i] = (int32_t)y[i];
+                    else if (p < 3) yh[i] = yh[i] * 256 + (int32_t)y[i];
+                    else if (p == 3) yl[i] = (int32_t)y[i];
+                    else yl[i] = yl[i] * 256 + (int32_t)y[i];
+                }
+            }
+            if (!live) continue;
+#pragma unroll
+            for (int i0 = 0; i0 < NC; i0 += 8) {
+                double v[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = i64_ldexp_exact((long long)yh[i0 + i] * 16777216LL + yl[i0 + i], eadj);
+                const int64_t n0 = (int64_t)tt * kTcN + colq * NC + i0;
                 if (a.f32) {
                     float* out = reinterpret_cast<float*>(a.beams) + ((size_t)b * a.n_dirs + slot) * a.N + n0;
-                    if (n0 + 16 <= a.L) {
+                    if (n0 + 8 <= a.L) {
 #pragma unroll
-                        for (int i = 0; i < 16; i += 4)
-                            *reinterpret_cast<float4*>(out + i) = make_float4((float)v[i], (float)v[i + 1], (float)v[i + 2], (float)v[i + 3]);
+                        for (int i = 0; i < 8; i += 4)
+                            *reinterpret_cast<float4*>(out + i) =
+                                make_float4((float)v[i], (float)v[i + 1], (float)v[i + 2], (float)v[i + 3]);
                     } else {
-                        for (int i = 0; i < 16; ++i) if (n0 + i < a.L) out[i] = (float)v[i];
+                        for (int i = 0; i < 8; ++i)
+                            if (n0 + i < a.L) out[i] = (float)v[i];
                     }
                 } else {
                     double* out = reinterpret_cast<double*>(a.beams) + ((size_t)b * a.n_dirs + slot) * a.N + n0;
-                    if (n0 + 16 <= a.L) {
+                    if (n0 + 8 <= a.L) {
 #pragma unroll
-                        for (int i = 0; i < 16; i += 2) *reinterpret_cast<double2*>(out + i) = make_double2(v[i], v[i + 1]);
+                        for (int i = 0; i < 8; i += 2) *reinterpret_cast<double2*>(out + i) = make_double2(v[i], v[i + 1]);
                     } else {
-                        for (int i = 0; i < 16; ++i) if (n0 + i < a.L) out[i] = v[i];
+                        for (int i = 0; i < 8; ++i)
+                            if (n0 + i < a.L) out[i] = v[i];
                     }
                 }
             }
         }
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        __syncthreads(); // TMEM drained and smem windows free before the next tile
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
@@ -304,9 +413,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
     }
 }
 
-size_t beamform_tc_smem_bytes(int pad) {
-    const size_t b = (size_t)12 * (kTcN + pad) * 16;
-    const size_t need = ((b + 127) & ~size_t(127)) + 2 * kTcRChunk * kABytes + 64 + 1024;
+size_t beamform_tc_smem_bytes(int rmax, int pad) {
+    const size_t need = (size_t)rmax * kABytes + kWin * (size_t)12 * (kTcN + pad) * 16 + 8 * (2 * kWin + 2 * kSlots) + 16;
     // >= 115 KB so at most one CTA (and one 512-column TMEM allocation) per SM
     return need > 118 * 1024 ? need : 118 * 1024;
 }
@@ -317,9 +425,15 @@ void launch_digits(const DigitArgs& a, int batch, cudaStream_t s) {
 }
 
 void launch_beamform_tc(const TcArgs& a, const TcSched& sched, int grid, cudaStream_t s) {
-    const size_t smem = beamform_tc_smem_bytes(a.pad);
-    cudaFuncSetAttribute((const void*)k_beamform_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = beamform_tc_smem_bytes(a.rmax, a.pad);
+    const cudaError_t e = cudaFuncSetAttribute((const void*)k_beamform_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "k_beamform_tc: %zu bytes of shared memory: %s\n", smem, cudaGetErrorString(e));
+        return;
+    }
     k_beamform_tc<<<grid, kTcThreads, smem, s>>>(a, sched);
+    const cudaError_t le = cudaPeekAtLastError();
+    if (le != cudaSuccess) fprintf(stderr, "k_beamform_tc launch: %s\n", cudaGetErrorString(le));
 }
 
 } // namespace snb

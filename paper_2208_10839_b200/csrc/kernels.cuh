@@ -108,9 +108,9 @@ double measure_fma_peak(int sms, bool f32);
 
 // ---- tensor-core delay-and-sum (beamform_tc.cu) ---------------------------
 constexpr int kTcM = 128;      // directions per cluster (MMA M)
-constexpr int kTcN = 80;       // time samples per tile (MMA N); 6 x 80 TMEM columns
+constexpr int kTcN = 64;       // time samples per tile (MMA N); TMEM ring of 8 x 64 columns
 constexpr int kTcSlices = 6;   // balanced base-256 digits of the 46-bit fixed-point samples
-constexpr int kTcRChunk = 8;   // shift values per A-operand chunk (double-buffered)
+constexpr int kTcRMax = 40;    // max shift values per cluster (A resident in smem: 4 KB each)
 struct DigitArgs {
     const double* filt;                // [B][32][Lp], sample n at H + n
     const unsigned long long* amax_bits; // [B]
@@ -122,17 +122,19 @@ struct DigitArgs {
 struct TcArgs {
     const int8_t* planes;              // as DigitArgs
     const uint8_t* resid;              // [C * 128][32] shift - base (0xFF: unused row)
-    const int32_t* R;                  // [C] shift values per cluster
+    const int32_t* R;                  // [C] shift values per cluster (<= kTcRMax)
+    const int32_t* cl_start;           // [C] first slot of the cluster
+    const int32_t* cl_size;            // [C] slots in the cluster (<= 128)
     const unsigned long long* amax_bits;
     void* beams;                       // [B][n_dirs][N] slot order, f64 or f32
     int64_t L, N, n_dirs;
-    int rows, pad, clusters, ntiles, batch, f32;
+    int rows, pad, clusters, ntiles, batch, f32, rmax;
 };
 constexpr int kTcMaxGrid = 512;
 struct TcSched { int start[kTcMaxGrid + 1]; }; // CTA k processes tiles [start[k], start[k+1])
 void launch_digits(const DigitArgs& a, int batch, cudaStream_t s);
 void launch_beamform_tc(const TcArgs& a, const TcSched& sched, int grid, cudaStream_t s);
-size_t beamform_tc_smem_bytes(int rmax);
+size_t beamform_tc_smem_bytes(int rmax, int pad);
 
 size_t demod_smem_bytes(int octets, int words);
 size_t fft_smem_bytes(int n, int real_bytes);

@@ -156,6 +156,9 @@ struct sn_workspace {
     int8_t* d_planes = nullptr;
     uint8_t* d_resid = nullptr;
     int32_t* d_tc_R = nullptr;
+    int32_t* d_tc_start = nullptr;
+    int32_t* d_tc_size = nullptr;
+    int tc_rmax = 0;
     int32_t* d_tc_base = nullptr;
     unsigned long long* d_amax = nullptr;
     FirTaps<double> taps64{};
@@ -190,7 +193,7 @@ struct sn_workspace {
                         (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot,  (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
                         (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32, (void*)d_tw_small, (void*)d_tw_small32, (void*)d_planes, (void*)d_resid,
-                        (void*)d_tc_R, (void*)d_tc_base, (void*)d_amax}) {
+                        (void*)d_tc_R, (void*)d_tc_base, (void*)d_amax, (void*)d_tc_start, (void*)d_tc_size}) {
             if (p) cudaFree(p);
         }
         if (h_in) cudaFreeHost(h_in);
@@ -355,9 +358,10 @@ struct sn_workspace {
         ck(cudaStreamSynchronize(stream), "setup sync");
     }
 
-    // Tensor-core delay-and-sum setup: clusters of kTcM consecutive slots, the
-    // per-cluster channel base shift b_i (min over the cluster), the residual
-    // bytes s - b_i per slot and the shift count R_c (beamform_tc.cu).
+    // Tensor-core delay-and-sum setup (beamform_tc.cu): clusters of <= kTcM
+    // consecutive slots cut greedily so that R_c (the largest per-channel
+    // shift span) stays <= kTcRMax; per cluster the channel base shifts b_i
+    // (min over the cluster) and per slot the residual bytes s - b_i.
     // SNB_BEAMFORMER=tiles selects the CUDA-core tiled kernel instead.
     void init_tensor_core_beamformer(int sms) {
         const char* env = std::getenv("SNB_BEAMFORMER");
@@ -365,28 +369,46 @@ struct sn_workspace {
         if (!tc) return;
         const Sizes& s = plan.sz;
         const uint64_t nd = s.n_dirs;
-        tc_clusters = (int)((nd + kTcM - 1) / kTcM);
-        std::vector<int32_t> base((size_t)tc_clusters * kCh, 0);
-        std::vector<uint8_t> resid((size_t)tc_clusters * kTcM * kCh, 0xFF);
-        tc_R.assign(tc_clusters, 1);
-        for (int c = 0; c < tc_clusters; ++c) {
-            const uint64_t s0 = (uint64_t)c * kTcM, s1 = std::min<uint64_t>(nd, s0 + kTcM);
+        std::vector<int32_t> base, start, size;
+        std::vector<uint8_t> resid;
+        tc_R.clear();
+        uint64_t s0 = 0;
+        while (s0 < nd) {
+            int lo[kCh], hi[kCh];
+            for (int i = 0; i < kCh; ++i) { lo[i] = 1 << 30; hi[i] = -(1 << 30); }
+            uint64_t s1 = s0;
             int R = 1;
-            for (int i = 0; i < kCh; ++i) {
-                int lo = 1 << 30, hi = -(1 << 30);
-                for (uint64_t sl = s0; sl < s1; ++sl) {
-                    lo = std::min(lo, plan.shifts[sl * kCh + i]);
-                    hi = std::max(hi, plan.shifts[sl * kCh + i]);
+            while (s1 < nd && s1 - s0 < (uint64_t)kTcM) {
+                int Rn = 1;
+                for (int i = 0; i < kCh; ++i) {
+                    const int v = plan.shifts[s1 * kCh + i];
+                    Rn = std::max(Rn, std::max(hi[i], v) - std::min(lo[i], v) + 1);
                 }
-                base[(size_t)c * kCh + i] = lo;
-                R = std::max(R, hi - lo + 1);
-                for (uint64_t sl = s0; sl < s1; ++sl) resid[sl * kCh + i] = (uint8_t)(plan.shifts[sl * kCh + i] - lo);
+                if (Rn > kTcRMax) break;
+                for (int i = 0; i < kCh; ++i) {
+                    const int v = plan.shifts[s1 * kCh + i];
+                    lo[i] = std::min(lo[i], v);
+                    hi[i] = std::max(hi[i], v);
+                }
+                R = Rn;
+                ++s1;
             }
-            if (R > 250) { tc = false; return; }
-            tc_R[c] = R;
+            const size_t c = tc_R.size();
+            tc_R.push_back(R);
+            start.push_back((int32_t)s0);
+            size.push_back((int32_t)(s1 - s0));
+            base.resize((c + 1) * kCh);
+            resid.resize((c + 1) * kTcM * kCh, 0xFF);
+            for (int i = 0; i < kCh; ++i) base[c * kCh + i] = lo[i];
+            for (uint64_t sl = s0; sl < s1; ++sl) {
+                for (int i = 0; i < kCh; ++i)
+                    resid[(c * kTcM + (sl - s0)) * kCh + i] = (uint8_t)(plan.shifts[sl * kCh + i] - lo[i]);
+            }
+            s0 = s1;
         }
-        const int rmax = *std::max_element(tc_R.begin(), tc_R.end());
-        tc_pad = (rmax + 6) & ~7; // >= rmax - 1, multiple of 8
+        tc_clusters = (int)tc_R.size();
+        tc_rmax = *std::max_element(tc_R.begin(), tc_R.end());
+        tc_pad = (tc_rmax + 6) & ~7; // >= rmax - 1, multiple of 8
         tc_ntiles = (int)((s.mf_len + kTcN - 1) / kTcN);
         tc_rows = tc_pad + tc_ntiles * kTcN;
         uint64_t& n = device_allocs;
@@ -394,10 +416,14 @@ struct sn_workspace {
         d_resid = dmalloc<uint8_t>(resid.size(), n);
         d_tc_R = dmalloc<int32_t>(tc_R.size(), n);
         d_tc_base = dmalloc<int32_t>(base.size(), n);
+        d_tc_start = dmalloc<int32_t>(start.size(), n);
+        d_tc_size = dmalloc<int32_t>(size.size(), n);
         d_amax = dmalloc<unsigned long long>(max_batch, n);
         upload(d_resid, resid, stream);
         upload(d_tc_R, tc_R, stream);
         upload(d_tc_base, base, stream);
+        upload(d_tc_start, start, stream);
+        upload(d_tc_size, size, stream);
         tc_grid = std::min(sms, kTcMaxGrid);
     }
 
@@ -452,6 +478,9 @@ struct sn_workspace {
             ta.planes = d_planes;
             ta.resid = d_resid;
             ta.R = d_tc_R;
+            ta.cl_start = d_tc_start;
+            ta.cl_size = d_tc_size;
+            ta.rmax = tc_rmax;
             ta.amax_bits = d_amax;
             ta.beams = d_beams;
             ta.L = (int64_t)z.mf_len;

@@ -221,7 +221,8 @@ def test_device_path_and_graph_replay_match_host_path(gpu):
         ws.process_device(dp.data_ptr(), B, out.data_ptr(), s.cuda_stream, graph=True)
     s.synchronize()
     assert np.array_equal(out.cpu().numpy(), host)
-    assert ws.last_launches() == 5
+    # demod, pre-MF, matched filter, digit planes, tensor-core delay-and-sum, envelope
+    assert ws.last_launches() == 6
 
 
 def test_decode_errors_on_device_workspace(gpu):
@@ -365,3 +366,39 @@ def test_full_size_batch_properties(gpu):
     one = sn.Workspace(cfg, device=0, max_batch=1)
     for i in (0, 7, 15):
         assert np.array_equal(one.process(ms[i]).energies, e[i])
+
+
+# ---------------------------------------------------------------------------
+# tensor-core delay-and-sum (beamform_tc.cu) against the CUDA-core tiled kernel
+# (channel-order FP64 sums, bit-identical beams) and the reference
+@pytest.mark.parametrize("name", ["small", "az181", "box1850", "hemi3000"])
+def test_tensor_core_beamformer_vs_tiled_and_reference(gpu, po, ref, name, monkeypatch):
+    sn = gpu
+    cfg = cfg_for(sn, name)
+    m = capture(sn, cfg, [(1.1, 0.3, 0.1 if name not in ("small", "az181") else 0.0, 0.7)], 0.01, 13)
+    monkeypatch.setenv("SNB_BEAMFORMER", "tiles")
+    ws_t = sn.Workspace(cfg, device=0)
+    monkeypatch.setenv("SNB_BEAMFORMER", "tc")
+    ws_c = sn.Workspace(cfg, device=0)
+    assert ws_c.last_launches() in (0, 6)
+    e_t, e_c = ws_t.process(m).energies, ws_c.process(m).energies
+    assert ws_c.last_launches() == 6 and ws_t.last_launches() == 5
+    want = ref.workspace(to_oracle(po, cfg)).process(m.packed)
+    check_f64(e_c, want)
+    check_f64(e_c, e_t)
+    assert ws_c.process(m).energies.tobytes() == e_c.tobytes()  # deterministic (integer MMA)
+
+
+def test_tensor_core_beamformer_scale_invariance(gpu):
+    # block floating point: the quantisation scale follows max|filt| of each
+    # capture, so silence and a strong echo in one batch do not interact
+    sn = gpu
+    cfg = cfg_for(sn, "small")
+    loud = capture(sn, cfg, [(0.9, 0.2, 0.0, 1.0)], 0.01, 4, seq=0)
+    quiet = capture(sn, cfg, [], 0.001, 5, seq=1)
+    ws1 = sn.Workspace(cfg, device=0)
+    ws2 = sn.Workspace(cfg, device=0, max_batch=2)
+    both = ws2.process_batch([loud, quiet])
+    assert np.array_equal(both[0].energies, ws1.process(loud).energies)
+    assert np.array_equal(both[1].energies, ws1.process(quiet).energies)
+    assert np.isfinite(both[1].energies).all() and both[1].energies.max() < both[0].energies.max()
