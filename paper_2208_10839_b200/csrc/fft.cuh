@@ -157,10 +157,10 @@ template <typename V> struct TwGlobal {
 constexpr int kTwSharedM = 4096;
 constexpr int kTwSharedCount = 16 * 4 + 256 * 4 + 65 + 64; // complex entries
 template <typename V> struct TwShared {
-    const V* t; // [t16: 16x4][t256: 256x4][A: 65][B: 64]
+    const V* t; // [t16: 4 x 16][t256: 4 x 256][A: 65][B: 64], exponent-major (lanes = k: conflict-free)
     __device__ __forceinline__ V w(int, int ns, int, int k, int e) const {
         const int le = e == 1 ? 0 : e == 2 ? 1 : e == 4 ? 2 : 3;
-        return ns == 16 ? t[k * 4 + le] : t[64 + k * 4 + le];
+        return ns == 16 ? t[le * 16 + k] : t[64 + le * 256 + k];
     }
     __device__ __forceinline__ V h(int k) const {
         const V a = t[64 + 1024 + (k >> 6)], b = t[64 + 1024 + 65 + (k & 63)];

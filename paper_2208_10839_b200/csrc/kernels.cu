@@ -297,9 +297,11 @@ __host__ __device__ int envelope_group_reals(int n, int phase_reals) {
 // the reciprocal root (~44 bits) and one on the root itself (<= 1 ulp),
 // instead of the correctly rounded library sequence; FP32: sqrtf.
 __device__ __forceinline__ double fast_sqrt(double x) {
-    // branch-free: the seed is clamped to the float range; x == 0 gives 0
-    const float xf = fminf(fmaxf((float)x, 1.17549435e-38f), 3.0e38f);
-    double r = (double)rsqrtf(xf);
+    // branch-free: FP64 approximate reciprocal root (MUFU.RSQ64H), one Newton
+    // step on the reciprocal, one on the root; x == 0 gives 0 (the seed input
+    // is clamped away from 0 so r stays finite)
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(fmax(x, 1e-300)));
     r = r * fma(-0.5 * x, r * r, 1.5);
     const double s = x * r;
     return fma(0.5 * r, fma(-s, s, x), s);
@@ -427,15 +429,19 @@ __global__ void __launch_bounds__(kThreads * G, SNB_ENV_MINB / G) k_envelope(Env
         R ev[NV];
         // all beam loads first (one batch of independent L2 reads), then the
         // shared Hilbert values and the roots, in place in the same registers
+        // branch-free when NV * kGroupThreads == N: every n < N is a valid
+        // beam (tail zero) and FFT-buffer index; values for n >= L are computed
+        // and never stored
+        constexpr bool kFull = NV * kGroupThreads == 2 * M;
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             const int n = tid + i * kGroupThreads;
-            ev[i] = n < L ? __ldg(src + n) : (R)0;
+            ev[i] = (kFull || n < 2 * M) ? __ldg(src + n) : (R)0;
         }
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             const int n = tid + i * kGroupThreads;
-            if (n < L) {
+            if (kFull || n < 2 * M) {
                 const R h = env[n + 2 * (n >> 5)];
                 ev[i] = fast_sqrt(ev[i] * ev[i] + h * h);
             }

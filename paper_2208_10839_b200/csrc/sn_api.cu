@@ -98,8 +98,8 @@ std::vector<double2> twiddles_small() {
     std::vector<double2> t;
     const int M = kTwSharedM, N = 2 * kTwSharedM;
     for (int ns : {16, 256}) {
-        for (int k = 0; k < ns; ++k) {
-            for (int ex : {1, 2, 4, 8}) t.push_back(e((long double)(M / (ns * 16)) * k * ex, M));
+        for (int ex : {1, 2, 4, 8}) {
+            for (int k = 0; k < ns; ++k) t.push_back(e((long double)(M / (ns * 16)) * k * ex, M));
         }
     }
     for (int a = 0; a <= 64; ++a) t.push_back(e(64.0L * a, N));
