@@ -122,27 +122,6 @@ __device__ __forceinline__ int bfp_exponent(unsigned long long amax_bits) {
     return ef ? ef - 1022 : 0;
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
-        "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr)
-        : "memory");
-}
-
-template <int NCOL>
-__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&v)[NCOL]) {
-    if constexpr (NCOL == 32) tmem_ld32(taddr, v);
-    else tmem_ld16(taddr, v);
-}
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(smem_dst)), "l"(gsrc) : "memory");
-}
 
 constexpr int kSlots = 512 / kTcN;            // TMEM ring of accumulator slots of kTcN columns
 constexpr int kWin = 3;                       // B window buffers (loads run kWin - 1 tiles ahead)
@@ -346,7 +325,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
         const int quarter = warp & 3, colq = warp >> 2;
         const int d = quarter * 32 + lane;
         constexpr int NC = kTcN / 4; // columns per thread
-        static_assert(NC == 16 || NC == 32, "epilogue column chunk");
+        static_assert(NC == 16, "epilogue column chunk: one 32x32b.x16 TMEM load");
         for (int g = 0; g < ntile; ++g) {
             const int t = t_beg + g;
             const int c = t / per_cb, rem = t - c * per_cb;
@@ -361,7 +340,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
                 mbar_wait(&sfull[sl], (uint32_t)((q / kSlots) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                 uint32_t y[NC];
-                tmem_ld_cols<NC>(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sl * kTcN + colq * NC), y);
+                tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sl * kTcN + colq * NC), y);
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
                 __syncwarp();

@@ -79,8 +79,8 @@ struct EnvArgs {
 // Polyphase smoothing FIR fast path (the reference's default composite
 // filter: 447 taps at stride 10 -> 10 phases x 45 taps): every thread owns
 // kFirR consecutive outputs (odd: bank-conflict free) over one half of the
-// phases; taps travel in the kernel parameters so every FMA takes its tap as
-// a constant-bank operand (no shared-memory tap loads).
+// phases; the phase-major taps travel in the kernel parameters and are copied
+// to shared memory once per CTA.
 constexpr int kFirR = 7;
 constexpr int kFirD = 10, kFirQ = 45;              // decimation, taps per phase
 constexpr int kFirTaps = kFirD * kFirQ;            // 450 (zero-padded)
