@@ -43,6 +43,11 @@ METRIC = "energyscapes/sec (32-mic, 3D grid) at 1/2/4/8 B200 + p50 latency vs CP
 UNIT = "energyscapes/s"
 BENCH_SCENE = [(1.5, 0.2, 0.0, 0.8), (3.0, -0.4, 0.1, 0.5)]  # bench.cpp:113-117
 GRIDS = {"horizontal90": 0, "box1850": 1, "hemisphere3000": 2, "az181": 3}
+# dense int8 tensor throughput of one B200 (2 ops per MAC): nominal 4.5 POPS;
+# scripts/micro/mma_rate.cu measured 4.49-4.58 POPS for M=128 x N=256 x K=32
+# tcgen05 kind::i8 on this pool (the M=128, N=64 shape the beamformer issues
+# is capped at ~2.9-3.0 POPS by the ~50-cycle per-instruction floor)
+TC_INT8_PEAK = 4500.0
 
 
 def parse_args():
@@ -358,6 +363,17 @@ def run_b200(args):
         f = kflops[k] * B
         kernels[k] = {"ms": ms, "tflops": f / (ms * 1e-3) / 1e12,
                       "frac": f / (ms * 1e-3) / 1e12 / peak}
+    bf = ws.beamformer_info()
+    if bf["kind"] == 1:
+        # tensor-core delay-and-sum: int8 MACs the MMAs execute per step (dense
+        # steering-matrix contraction over (shift, channel), six digit planes)
+        macs = bf["sum_R"] * bf["ntiles"] * bf["slices"] * bf["m"] * bf["n"] * bf["k"] * B
+        tops = 2 * macs / (stage_avg["beamform"] * 1e-3) / 1e12
+        kernels["beamform"].update({
+            "path": "tcgen05 kind::i8 (k_digits + k_beamform_tc)", "int8_tops_executed": tops,
+            "int8_peak_tops": TC_INT8_PEAK, "tensor_frac": tops / TC_INT8_PEAK,
+            "mma": {"m": bf["m"], "n": bf["n"], "k": bf["k"], "clusters": bf["clusters"],
+                    "sum_R": bf["sum_R"], "slices": bf["slices"]}})
     dom = max(stage_avg, key=stage_avg.get)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")

@@ -230,6 +230,21 @@ sn_status sn_workspace_process_device_graph(sn_workspace* ws, const uint8_t* d_p
 sn_status sn_workspace_set_profiling(sn_workspace* ws, int enable);
 sn_status sn_workspace_stage_times(sn_workspace* ws, float* ms5);
 
+/* Delay-and-sum schedule of a device workspace. kind 1: tensor-core path
+ * (tcgen05 int8 MMAs over direction clusters, beamform_tc.cu); kind 0: the
+ * CUDA-core tiled kernel (SNB_BEAMFORMER=tiles). For kind 1, the MMA work of
+ * one capture is sum_R * ntiles * slices MMAs of m x n x k int8 MACs. */
+typedef struct sn_beamformer_info {
+    int32_t kind;
+    int32_t clusters;     /* direction clusters (<= m directions each)        */
+    int64_t sum_R;        /* sum over clusters of the shift values R_c        */
+    int32_t max_R;
+    int32_t ntiles;       /* time tiles of n samples per capture              */
+    int32_t slices;       /* int8 digit planes of the 46-bit samples          */
+    int32_t m, n, k;      /* MMA shape                                        */
+} sn_beamformer_info;
+sn_status sn_workspace_beamformer_info(const sn_workspace* ws, sn_beamformer_info* info);
+
 /* FMA-throughput microbenchmark on `device` (TFLOP/s, FMA = 2 flops); the
  * roofline denominator for CUDA-core kernels (no tensor cores involved). */
 sn_status sn_measure_fp_peak(int device, int precision, double* tflops);

@@ -140,6 +140,12 @@ _lib: Optional[C.CDLL] = None
 STAGES = ("demod", "premf", "matched_filter", "beamform", "envelope")
 
 
+class _BfInfo(C.Structure):  # sn_beamformer_info
+    _fields_ = [("kind", C.c_int32), ("clusters", C.c_int32), ("sum_R", C.c_int64), ("max_R", C.c_int32),
+                ("ntiles", C.c_int32), ("slices", C.c_int32), ("m", C.c_int32), ("n", C.c_int32),
+                ("k", C.c_int32)]
+
+
 def lib() -> C.CDLL:
     """Load libsonarnet_b200.so (raises if it was not built — no fallback)."""
     global _lib
@@ -175,6 +181,7 @@ def lib() -> C.CDLL:
     L.sn_workspace_set_profiling.argtypes = [vp, C.c_int]
     L.sn_workspace_stage_times.argtypes = [vp, vp]
     L.sn_measure_fp_peak.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
+    L.sn_workspace_beamformer_info.argtypes = [vp, C.POINTER(_BfInfo)]
     _lib = L
     return L
 
@@ -465,6 +472,13 @@ class Workspace:
         out = np.empty(n.value, np.float64)
         _check(lib().sn_workspace_table(self._h, which, out.ctypes.data, n.value, C.byref(n)))
         return out
+
+    def beamformer_info(self) -> dict:
+        """Delay-and-sum schedule (sn_workspace_beamformer_info): kind 1 =
+        tensor-core path with its cluster / tile / MMA-shape figures."""
+        info = _BfInfo()
+        _check(lib().sn_workspace_beamformer_info(self._h, C.byref(info)))
+        return {f: getattr(info, f) for f, _ in _BfInfo._fields_}
 
     def set_profiling(self, enable: bool = True):
         _check(lib().sn_workspace_set_profiling(self._h, int(enable)))

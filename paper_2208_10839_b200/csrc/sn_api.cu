@@ -363,15 +363,19 @@ struct sn_workspace {
     // shift span) stays <= kTcRMax; per cluster the channel base shifts b_i
     // (min over the cluster) and per slot the residual bytes s - b_i.
     // SNB_BEAMFORMER=tiles selects the CUDA-core tiled kernel instead.
-    void init_tensor_core_beamformer(int sms) {
+    std::vector<int32_t> tc_base, tc_start, tc_size;
+    std::vector<uint8_t> tc_resid;
+    void plan_tensor_core_beamformer() {
         const char* env = std::getenv("SNB_BEAMFORMER");
         tc = !(env && std::string(env) == "tiles");
         if (!tc) return;
         const Sizes& s = plan.sz;
         const uint64_t nd = s.n_dirs;
-        std::vector<int32_t> base, start, size;
-        std::vector<uint8_t> resid;
         tc_R.clear();
+        tc_base.clear();
+        tc_start.clear();
+        tc_size.clear();
+        tc_resid.clear();
         uint64_t s0 = 0;
         while (s0 < nd) {
             int lo[kCh], hi[kCh];
@@ -395,14 +399,14 @@ struct sn_workspace {
             }
             const size_t c = tc_R.size();
             tc_R.push_back(R);
-            start.push_back((int32_t)s0);
-            size.push_back((int32_t)(s1 - s0));
-            base.resize((c + 1) * kCh);
-            resid.resize((c + 1) * kTcM * kCh, 0xFF);
-            for (int i = 0; i < kCh; ++i) base[c * kCh + i] = lo[i];
+            tc_start.push_back((int32_t)s0);
+            tc_size.push_back((int32_t)(s1 - s0));
+            tc_base.resize((c + 1) * kCh);
+            tc_resid.resize((c + 1) * kTcM * kCh, 0xFF);
+            for (int i = 0; i < kCh; ++i) tc_base[c * kCh + i] = lo[i];
             for (uint64_t sl = s0; sl < s1; ++sl) {
                 for (int i = 0; i < kCh; ++i)
-                    resid[(c * kTcM + (sl - s0)) * kCh + i] = (uint8_t)(plan.shifts[sl * kCh + i] - lo[i]);
+                    tc_resid[(c * kTcM + (sl - s0)) * kCh + i] = (uint8_t)(plan.shifts[sl * kCh + i] - lo[i]);
             }
             s0 = s1;
         }
@@ -411,19 +415,23 @@ struct sn_workspace {
         tc_pad = (tc_rmax + 6) & ~7; // >= rmax - 1, multiple of 8
         tc_ntiles = (int)((s.mf_len + kTcN - 1) / kTcN);
         tc_rows = tc_pad + tc_ntiles * kTcN;
+    }
+
+    void init_tensor_core_beamformer(int sms) {
+        if (!tc) return;
         uint64_t& n = device_allocs;
         d_planes = dmalloc<int8_t>(max_batch * (uint64_t)tc_clusters * 12 * tc_rows * 16, n);
-        d_resid = dmalloc<uint8_t>(resid.size(), n);
+        d_resid = dmalloc<uint8_t>(tc_resid.size(), n);
         d_tc_R = dmalloc<int32_t>(tc_R.size(), n);
-        d_tc_base = dmalloc<int32_t>(base.size(), n);
-        d_tc_start = dmalloc<int32_t>(start.size(), n);
-        d_tc_size = dmalloc<int32_t>(size.size(), n);
+        d_tc_base = dmalloc<int32_t>(tc_base.size(), n);
+        d_tc_start = dmalloc<int32_t>(tc_start.size(), n);
+        d_tc_size = dmalloc<int32_t>(tc_size.size(), n);
         d_amax = dmalloc<unsigned long long>(max_batch, n);
-        upload(d_resid, resid, stream);
+        upload(d_resid, tc_resid, stream);
         upload(d_tc_R, tc_R, stream);
-        upload(d_tc_base, base, stream);
-        upload(d_tc_start, start, stream);
-        upload(d_tc_size, size, stream);
+        upload(d_tc_base, tc_base, stream);
+        upload(d_tc_start, tc_start, stream);
+        upload(d_tc_size, tc_size, stream);
         tc_grid = std::min(sms, kTcMaxGrid);
     }
 
@@ -698,6 +706,7 @@ sn_status sn_workspace_create(const sn_pipeline_config* cfg, int device, uint64_
         ws->device = device;
         ws->max_batch = std::max<uint64_t>(1, max_batch);
         ws->f32 = cfg->precision == SN_PRECISION_F32;
+        ws->plan_tensor_core_beamformer();
         if (cfg->precision != SN_PRECISION_F64 && cfg->precision != SN_PRECISION_F32) {
             config_error("pipeline: unknown precision mode");
         }
@@ -882,6 +891,23 @@ sn_status sn_workspace_stage_times(sn_workspace* ws, float* ms5) {
         DeviceGuard g(ws->device);
         ck(cudaEventSynchronize(ws->ev[5]), "event sync");
         for (int i = 0; i < 5; ++i) ck(cudaEventElapsedTime(&ms5[i], ws->ev[i], ws->ev[i + 1]), "elapsed");
+    });
+}
+
+sn_status sn_workspace_beamformer_info(const sn_workspace* ws, sn_beamformer_info* info) {
+    return guarded([&] {
+        if (!ws || !info) argument_error("null argument");
+        *info = sn_beamformer_info{};
+        info->kind = ws->tc ? 1 : 0;
+        if (!ws->tc) return;
+        info->clusters = ws->tc_clusters;
+        for (int32_t r : ws->tc_R) info->sum_R += r;
+        info->max_R = ws->tc_rmax;
+        info->ntiles = ws->tc_ntiles;
+        info->slices = kTcSlices;
+        info->m = kTcM;
+        info->n = kTcN;
+        info->k = 32;
     });
 }
 

@@ -27,6 +27,7 @@ METRICS = [
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2_throughput_pct"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_throughput_pct"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64_pipe_pct"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor_pipe_pct"),
     ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "fma_pipe_pct"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_active_pct"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved_occupancy_pct"),
@@ -90,7 +91,8 @@ def read_launches(path):
 
 
 def short(name):
-    for k in ("k_demod", "k_premf", "k_matched_filter", "k_beamform_tiles", "k_envelope", "k_rfft_forward"):
+    for k in ("k_demod", "k_premf", "k_matched_filter", "k_beamform_tiles", "k_beamform_tc", "k_digits",
+              "k_envelope", "k_rfft_forward"):
         if k in name:
             return k
     return name.split("(")[0][-40:]
@@ -103,7 +105,8 @@ def main():
     tpath = os.path.join(PROF, "traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     stage_of = {"k_demod": "demod", "k_premf": "premf", "k_matched_filter": "matched_filter",
-                "k_beamform_tiles": "beamform", "k_envelope": "envelope"}
+                "k_beamform_tiles": "beamform", "k_digits": "beamform", "k_beamform_tc": "beamform",
+                "k_envelope": "envelope"}
     for i in range(0, len(items), 3):
         rep, launches, key = items[i], items[i + 1], items[i + 2]
         ks = read_full(rep)
@@ -114,12 +117,14 @@ def main():
               "serialised: compare shares, not absolutes).", "", "## Launch list (one process() step)", "",
               "| kernel | grid launches | time (us) | share |", "|---|---|---|---|"]
         ours = [(short(n), t) for n, t in ls if short(n) in stage_of]
-        # last complete pipeline pass (5 kernels)
-        last = ours[-5:]
+        # last complete pipeline pass (from the last k_demod on)
+        starts = [i for i, (n, _) in enumerate(ours) if n == "k_demod"]
+        last = ours[starts[-1]:] if starts else ours
         tot = sum(t for _, t in last)
         for n, t in last:
             md.append(f"| {n} | 1 | {t * 1e6:.1f} | {t / tot * 100:.1f}% |")
         md += ["", "## Per-kernel metrics (full capture)", ""]
+        seen = {}
         for k in ks:
             name = short(k["kernel"])
             md.append(f"### {name}")
@@ -132,7 +137,10 @@ def main():
                       ", ".join(f"{s} {v:.2f}" for s, v in list(k['stalls'].items())[:6]))
             md.append("")
             if name in stage_of and "dram_read" in k:
-                traffic[f"{key}/{stage_of[name]}"] = k.get("dram_read", 0) + k.get("dram_write", 0)
+                tk = f"{key}/{stage_of[name]}"
+                seen.setdefault(tk, 0.0)
+                seen[tk] += k.get("dram_read", 0) + k.get("dram_write", 0)
+                traffic[tk] = seen[tk]
         open(os.path.join(PROF, f"{tag}_{key.replace('/', '_')}_ncu.md"), "w").write("\n".join(md) + "\n")
     json.dump(traffic, open(tpath, "w"), indent=1, sort_keys=True)
     print("wrote", tpath)

@@ -199,3 +199,20 @@ def test_dims_of_standard_configs(sn):
     assert (t["frames"], t["range_bins"]) == (13200, 58)
     s = sn.default_pipeline_config().copy(max_range=1.5).dims()
     assert (s["frames"], s["mf_samples"], s["range_bins"], s["env_fft_size"]) == (53000, 2650, 196, 4096)
+
+
+def test_tensor_core_beamformer_schedule(sn, monkeypatch):
+    # host-side cluster schedule of the tcgen05 delay-and-sum (beamform_tc.cu):
+    # every direction in one cluster of <= 128 slots with <= 40 shift values
+    import math
+    for kind in (0, 1, 2):
+        cfg = sn.default_pipeline_config(kind)
+        ws = sn.Workspace(cfg, device=-1)
+        info = ws.beamformer_info()
+        n = ws.n_dirs
+        assert info["kind"] == 1 and info["m"] == 128 and info["k"] == 32 and info["slices"] == 6
+        assert math.ceil(n / 128) <= info["clusters"] <= n
+        assert 1 <= info["max_R"] <= 40 and info["sum_R"] <= info["clusters"] * info["max_R"]
+        assert info["ntiles"] == math.ceil(ws.dims["mf_samples"] / info["n"])
+    monkeypatch.setenv("SNB_BEAMFORMER", "tiles")
+    assert sn.Workspace(sn.default_pipeline_config(2), device=-1).beamformer_info()["kind"] == 0
