@@ -245,6 +245,26 @@ typedef struct sn_beamformer_info {
 } sn_beamformer_info;
 sn_status sn_workspace_beamformer_info(const sn_workspace* ws, sn_beamformer_info* info);
 
+/* ---- wire format (protocol.md) ------------------------------------------
+ * The central node's traffic around Workspace::process: raw-measurement frames
+ * in (wire::measurement_frame, wire.cpp:251-259), processed-image frames out
+ * (wire::image_frame(image_to_bytes(img), seq), wire.cpp:268-276,
+ * pipeline.cpp:109-125). CRC-32 as wire::crc32 (wire.cpp:58-63). */
+uint32_t sn_crc32(const uint8_t* bytes, uint64_t n);
+sn_status sn_measurement_frame(const sn_raw_measurement* m, uint8_t* out, uint64_t capacity, uint64_t* n_out);
+/* Size of one processed-image frame of this workspace's configuration. */
+uint64_t sn_workspace_image_frame_bytes(const sn_workspace* ws);
+/* Process `count` received frames (central_node.cpp:130-160, 238-270):
+ * per frame i, out + i * slot_bytes receives out_lens[i] bytes and status[i] is
+ *   SN_OK          the processed-image frame (AIMG payload, CRC) — encoded and
+ *                  CRC'd on the GPU, input CRC verified on the GPU
+ *   SN_ERR_DECODE  process() rejected the measurement: wire::error_frame
+ *   SN_ERR_IO      malformed, CRC mismatch or not a measurement: discarded (0 bytes)
+ * slot_bytes >= sn_workspace_image_frame_bytes(ws). */
+sn_status sn_workspace_process_frames(sn_workspace* ws, const uint8_t* const* frames, const uint64_t* lens,
+                                      uint64_t count, uint8_t* out, uint64_t slot_bytes, uint64_t* out_lens,
+                                      int32_t* status);
+
 /* FMA-throughput microbenchmark on `device` (TFLOP/s, FMA = 2 flops); the
  * roofline denominator for CUDA-core kernels (no tensor cores involved). */
 sn_status sn_measure_fp_peak(int device, int precision, double* tflops);

@@ -74,6 +74,12 @@ typedef struct orc_scene {
 
 /* status: 0 ok, 1 config, 2 argument, 3 decode, 4 io, 6 other */
 
+/* wire format (protocol.md, wire.cpp) */
+uint32_t ref_crc32(const uint8_t* bytes, uint64_t n);
+int ref_measurement_frame(const orc_measurement* m, uint8_t* out, uint64_t cap, uint64_t* n_out);
+int ref_ws_process_frame(void* ws, const uint8_t* frame, uint64_t len, uint8_t* out, uint64_t cap,
+                         uint64_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,7 @@ class OracleError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"[{status}] {msg}")
         self.status = status
+        self.msg = msg
 
 
 @dataclass
@@ -156,6 +157,12 @@ class Ref:
         L.ref_default_array.argtypes = [C.c_uint64, C.c_void_p]
         L.ref_direction_grid.argtypes = [C.c_int, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
         L.ref_default_config.argtypes = [C.c_int, C.POINTER(OrcConfig), C.c_void_p, C.c_uint64]
+        L.ref_crc32.restype = C.c_uint32
+        L.ref_crc32.argtypes = [C.c_void_p, C.c_uint64]
+        L.ref_measurement_frame.argtypes = [C.POINTER(OrcMeasurement), C.c_void_p, C.c_uint64,
+                                            C.POINTER(C.c_uint64)]
+        L.ref_ws_process_frame.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                                           C.POINTER(C.c_uint64)]
 
     def _check(self, rc):
         if rc != 0:
@@ -205,6 +212,20 @@ class Ref:
     def workspace(self, cfg: Config) -> "RefWorkspace":
         return RefWorkspace(self, cfg)
 
+    # --- wire format (wire.cpp) ----------------------------------------
+    def crc32(self, data) -> int:
+        b = np.ascontiguousarray(np.frombuffer(bytes(data), np.uint8) if not isinstance(data, np.ndarray) else data,
+                                 dtype=np.uint8)
+        return int(self.lib.ref_crc32(b.ctypes.data, b.size))
+
+    def measurement_frame(self, packed, frames, pdm_rate, serial=1, ts=0, seq=0, channels=32) -> bytes:
+        m, _k = measurement_struct(packed, frames, pdm_rate, serial, ts, seq, channels)
+        n = C.c_uint64(0)
+        self._check(self.lib.ref_measurement_frame(C.byref(m), None, 0, C.byref(n)))
+        out = np.zeros(n.value, np.uint8)
+        self._check(self.lib.ref_measurement_frame(C.byref(m), out.ctypes.data, out.size, C.byref(n)))
+        return out.tobytes()
+
     def throughput(self, cfg: Config, pool: np.ndarray, threads: int, calls_per_worker: int):
         st, _keep = cfg.to_struct()
         pool = np.ascontiguousarray(pool, dtype=np.uint8)
@@ -251,6 +272,17 @@ class RefWorkspace:
         out = np.zeros((self.dims["n_dirs"], self.dims["range_bins"]), np.float32)
         self.ref._check(self.ref.lib.ref_ws_process(self.h, C.byref(m), out.ctypes.data))
         return out
+
+    def process_frame(self, frame: bytes) -> bytes:
+        """Central-node path for one received frame: decode_packet (CRC) ->
+        decode_raw_measurement -> process -> wire::image_frame(image, seq)."""
+        f = np.frombuffer(frame, np.uint8)
+        cap = 64 + 8 * self.dims["n_dirs"] + 4 * self.dims["n_dirs"] * self.dims["range_bins"] + 64
+        out = np.zeros(cap, np.uint8)
+        n = C.c_uint64(0)
+        self.ref._check(self.ref.lib.ref_ws_process_frame(self.h, f.ctypes.data, f.size, out.ctypes.data,
+                                                          out.size, C.byref(n)))
+        return out[: n.value].tobytes()
 
     def stage(self, which: int):
         d = self.dims

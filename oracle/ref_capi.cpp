@@ -75,6 +75,9 @@ int guarded(F&& f) {
     } catch (const DecodeError& e) {
         g_error = e.what();
         return 3;
+    } catch (const ProtocolError& e) { // CLI maps protocol errors to 3 as well (errors.hpp:9)
+        g_error = e.what();
+        return 3;
     } catch (const IoError& e) {
         g_error = e.what();
         return 4;
@@ -402,6 +405,35 @@ int ref_throughput(const orc_config* c, const uint8_t* pool, uint64_t pool_n, in
         }
         stats[0] = std::chrono::duration<double>(t1 - t0).count();
         stats[1] = static_cast<double>(calls_per_worker) * threads;
+    });
+}
+
+// ---- wire format (protocol.md; wire.cpp) -----------------------------------
+uint32_t ref_crc32(const uint8_t* bytes, uint64_t n) { return wire::crc32({bytes, static_cast<size_t>(n)}); }
+
+// wire::measurement_frame (wire.cpp:251-259): the frame a sensor node sends.
+int ref_measurement_frame(const orc_measurement* m, uint8_t* out, uint64_t cap, uint64_t* n_out) {
+    return guarded([&] {
+        const auto f = wire::measurement_frame(to_measurement(*m));
+        copy_out(f, out, cap, n_out);
+    });
+}
+
+// The central node's processing of one received frame (central_node.cpp:
+// decode_packet -> decode_raw_measurement -> Workspace::process ->
+// wire::image_frame(image, seq)). Returns the reference's error classes
+// (3: decode/protocol); a CRC mismatch throws ProtocolError from decode_packet.
+int ref_ws_process_frame(void* p, const uint8_t* frame, uint64_t len, uint8_t* out, uint64_t cap,
+                         uint64_t* n_out) {
+    return guarded([&] {
+        auto* ws = static_cast<Workspace*>(p);
+        size_t consumed = 0;
+        const auto pkt = wire::decode_packet({frame, static_cast<size_t>(len)}, &consumed);
+        if (pkt.msg_type != wire::MsgType::raw_measurement) throw DecodeError("not a raw measurement frame");
+        const auto m = wire::decode_raw_measurement(pkt.payload);
+        const auto img = ws->process(m);
+        const auto f = wire::image_frame(img, m.seq);
+        copy_out(f, out, cap, n_out);
     });
 }
 

@@ -33,7 +33,7 @@ __all__ = [
     "GridKind", "Precision", "PipelineConfig", "RawMeasurement", "AcousticImage", "Reflector",
     "Scene", "Workspace", "default_pipeline_config", "direction_grid", "default_array",
     "synthesize_measurement", "SonarError", "ConfigError", "ArgumentError", "DecodeError",
-    "IoError", "CudaError", "lib",
+    "IoError", "CudaError", "lib", "crc32", "measurement_frame",
 ]
 
 
@@ -182,6 +182,13 @@ def lib() -> C.CDLL:
     L.sn_workspace_stage_times.argtypes = [vp, vp]
     L.sn_measure_fp_peak.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
     L.sn_workspace_beamformer_info.argtypes = [vp, C.POINTER(_BfInfo)]
+    L.sn_crc32.restype = C.c_uint32
+    L.sn_crc32.argtypes = [vp, u64]
+    L.sn_measurement_frame.argtypes = [C.POINTER(_Measurement), vp, u64, C.POINTER(u64)]
+    L.sn_workspace_image_frame_bytes.restype = u64
+    L.sn_workspace_image_frame_bytes.argtypes = [vp]
+    L.sn_workspace_process_frames.argtypes = [vp, C.POINTER(C.c_void_p), C.POINTER(u64), u64, vp, u64,
+                                              C.POINTER(u64), C.POINTER(C.c_int32)]
     _lib = L
     return L
 
@@ -200,6 +207,22 @@ def measure_fp_peak(device: int = 0, precision: Precision = Precision.f64) -> fl
 
 
 # ---------------------------------------------------------------------------
+def crc32(data) -> int:
+    """wire::crc32 (wire.cpp:58-63), host implementation of the C ABI."""
+    b = np.ascontiguousarray(np.frombuffer(bytes(data), np.uint8))
+    return int(lib().sn_crc32(b.ctypes.data if b.size else None, b.size))
+
+
+def measurement_frame(m: "RawMeasurement") -> bytes:
+    """wire::measurement_frame (wire.cpp:251-259): the frame a sensor sends."""
+    st, _keep = m._struct()
+    n = C.c_uint64(0)
+    _check(lib().sn_measurement_frame(C.byref(st), None, 0, C.byref(n)))
+    out = np.empty(n.value, np.uint8)
+    _check(lib().sn_measurement_frame(C.byref(st), out.ctypes.data, out.size, C.byref(n)))
+    return out.tobytes()
+
+
 def default_array(seed: int = 42) -> np.ndarray:
     """geometry.cpp:69-96 — 32 x 3 microphone positions (m)."""
     out = np.zeros(96, np.float64)
@@ -418,6 +441,28 @@ class Workspace:
         return [AcousticImage(m.sensor_serial, m.timestamp_us, np.array(self._cfg.directions),
                               self.dims["range_bin_size"], self.bins, out[i])
                 for i, m in enumerate(ms)]
+
+    @property
+    def image_frame_bytes(self) -> int:
+        """Size of one processed-image frame (wire::image_frame) of this config."""
+        return int(lib().sn_workspace_image_frame_bytes(self._h))
+
+    def process_frames(self, frames: Sequence[bytes], out: Optional[np.ndarray] = None):
+        """The central node's path for received frames (sn_workspace_process_frames):
+        returns [(status, frame_bytes)] — status 0 with the processed-image
+        frame, DecodeError.status with the reference's error frame, IoError.status
+        (discarded: malformed / CRC mismatch / not a measurement) with b""."""
+        n = len(frames)
+        slot = self.image_frame_bytes
+        keep = [np.frombuffer(f, np.uint8) for f in frames]
+        ptrs = (C.c_void_p * max(1, n))(*[k.ctypes.data for k in keep])
+        lens = (C.c_uint64 * max(1, n))(*[k.size for k in keep])
+        if out is None or out.size < n * slot:
+            out = np.empty(max(1, n) * slot, np.uint8)
+        olen = (C.c_uint64 * max(1, n))()
+        st = (C.c_int32 * max(1, n))()
+        _check(lib().sn_workspace_process_frames(self._h, ptrs, lens, n, out.ctypes.data, slot, olen, st))
+        return [(int(st[i]), out[i * slot:i * slot + olen[i]].tobytes()) for i in range(n)]
 
     def process_packed_host(self, packed: np.ndarray, out: np.ndarray):
         """Fast host path for B equal-sized captures already packed as

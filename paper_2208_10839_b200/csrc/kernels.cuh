@@ -106,6 +106,34 @@ void launch_beamform(const double* filt, double* beams, const int32_t* shifts, i
 
 double measure_fma_peak(int sms, bool f32);
 
+// ---- wire-format frames on the GPU (frames.cu) ------------------------------
+constexpr int kCrcChunk = 2048;     // bytes per thread (multiple of 4)
+constexpr int kCrcShiftMats = 48;   // A_{2^k}, k < 48: messages up to 2^48 bytes
+struct CrcTables {
+    const uint32_t* slice;          // [4][256] slicing-by-4 tables
+    const uint32_t* shift;          // [kCrcShiftMats][32] columns of A_{2^k}
+};
+struct FrameIds {                   // per-capture header fields
+    uint32_t serial;
+    uint64_t ts, seq;
+};
+struct ImageFrameArgs {
+    const float* energies;          // [count][cells] direction order
+    const uint8_t* tpl;             // header + direction table template (tpl_len bytes)
+    const FrameIds* ids;            // [count]
+    uint8_t* frames;                // [count][frame_stride]
+    uint32_t* acc;                  // [count] CRC accumulators (zeroed)
+    uint64_t cells, tpl_len, frame_len, frame_stride;
+};
+void launch_crc_partial(const uint8_t* base, uint64_t stride, uint64_t n, uint64_t count, const CrcTables& ct,
+                        uint32_t* acc, cudaStream_t s);
+void launch_encode_image_frames(const ImageFrameArgs& a, uint64_t count, const CrcTables& ct, cudaStream_t s);
+void launch_crc_finalize(uint32_t* acc, uint32_t k_n, uint64_t count, uint8_t* out, uint64_t stride, uint64_t n,
+                         bool store, int32_t* ok, cudaStream_t s);
+uint32_t crc32_host(const uint8_t* p, uint64_t n);
+void crc_tables_host(uint32_t* slice, uint32_t* shift);
+uint32_t crc_init_term(const uint32_t* shift, uint64_t n);
+
 // ---- tensor-core delay-and-sum (beamform_tc.cu) ---------------------------
 constexpr int kTcM = 128;      // directions per cluster (MMA M)
 constexpr int kTcN = 64;       // time samples per tile (MMA N); TMEM ring of 8 x 64 columns

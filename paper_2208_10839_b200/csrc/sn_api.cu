@@ -149,6 +149,22 @@ struct sn_workspace {
     int demod_grid = 0;
     size_t demod_smem = 0, mf_smem = 0, dir_smem = 0;
     int dir_grid = 0, halo = 0, tile = 0, fir_q = 0, phase_len = 0, fir_fast = 0;
+    // wire-format frames (frames.cu)
+    uint32_t* d_crc_slice = nullptr;
+    uint32_t* d_crc_shift = nullptr;
+    std::vector<uint32_t> h_crc_shift;
+    uint8_t* d_img_tpl = nullptr;
+    uint64_t img_tpl_len = 0, img_frame_len = 0, img_frame_stride = 0;
+    uint64_t in_frame_len = 0, in_frame_stride = 0;
+    uint8_t* d_frames_out = nullptr;
+    uint8_t* h_frames_out = nullptr;
+    uint8_t* d_frames_in = nullptr;
+    uint8_t* h_frames_in = nullptr;
+    FrameIds* d_ids = nullptr;
+    FrameIds* h_ids = nullptr;
+    uint32_t* d_crc_acc = nullptr;   // [2][max_batch]: inputs, outputs
+    int32_t* d_crc_ok = nullptr;
+    int32_t* h_crc_ok = nullptr;
     // tensor-core beamformer (beamform_tc.cu)
     bool tc = false;
     int tc_clusters = 0, tc_pad = 0, tc_rows = 0, tc_ntiles = 0, tc_grid = 0;
@@ -193,10 +209,15 @@ struct sn_workspace {
                         (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot,  (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
                         (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32, (void*)d_tw_small, (void*)d_tw_small32, (void*)d_planes, (void*)d_resid,
-                        (void*)d_tc_R, (void*)d_tc_base, (void*)d_amax, (void*)d_tc_start, (void*)d_tc_size}) {
+                        (void*)d_tc_R, (void*)d_tc_base, (void*)d_amax, (void*)d_tc_start, (void*)d_tc_size,
+                        (void*)d_crc_slice, (void*)d_crc_shift, (void*)d_img_tpl, (void*)d_frames_out,
+                        (void*)d_frames_in, (void*)d_ids, (void*)d_crc_acc, (void*)d_crc_ok}) {
             if (p) cudaFree(p);
         }
         if (h_in) cudaFreeHost(h_in);
+        for (void* p : {(void*)h_frames_out, (void*)h_frames_in, (void*)h_ids, (void*)h_crc_ok}) {
+            if (p) cudaFreeHost(p);
+        }
         if (h_out) cudaFreeHost(h_out);
         if (stream) cudaStreamDestroy(stream);
         if (prev >= 0) cudaSetDevice(prev);
@@ -355,8 +376,66 @@ struct sn_workspace {
             dir_grid = sms * envelope_blocks_per_sm(f32, (int)s.env_fft, dir_smem);
         }
         mf_smem = fft_smem_bytes((int)s.mf_fft, sizeof(double));
+        init_frames();
         ck(cudaStreamSynchronize(stream), "setup sync");
     }
+
+    // ---- wire-format frames (protocol.md): CRC tables, the processed-image
+    // frame template (packet header + AIMG header + direction table,
+    // pipeline.cpp:109-125, wire.cpp:66-81,268-276) and frame buffers
+    static void put(std::vector<uint8_t>& v, const void* p, size_t n) {
+        const uint8_t* b = static_cast<const uint8_t*>(p);
+        v.insert(v.end(), b, b + n);
+    }
+    std::vector<uint8_t> image_template() const {
+        const Sizes& z = plan.sz;
+        std::vector<uint8_t> t;
+        const uint32_t magic = 0x45525449u, aimg = 0x41494D47u, zero32 = 0;
+        const uint16_t version = 1, msg = 2;
+        const uint64_t zero64 = 0;
+        const uint64_t payload = 34 + 8 * z.n_dirs + 4 * z.n_dirs * z.bins;
+        put(t, &magic, 4); put(t, &version, 2); put(t, &msg, 2); put(t, &zero32, 4);
+        put(t, &zero64, 8); put(t, &zero64, 8); put(t, &payload, 8);
+        const uint32_t nd = (uint32_t)z.n_dirs, nb = (uint32_t)z.bins;
+        const uint16_t iv = 1;
+        put(t, &aimg, 4); put(t, &iv, 2); put(t, &zero32, 4); put(t, &zero64, 8);
+        put(t, &nd, 4); put(t, &nb, 4); put(t, &z.range_bin_size, 8);
+        for (uint64_t d = 0; d < z.n_dirs; ++d) {
+            const float az = (float)plan.directions[2 * d], el = (float)plan.directions[2 * d + 1];
+            put(t, &az, 4); put(t, &el, 4);
+        }
+        return t;
+    }
+    void init_frames() {
+        const Sizes& z = plan.sz;
+        uint64_t& n = device_allocs;
+        std::vector<uint32_t> slice(1024);
+        h_crc_shift.assign((size_t)kCrcShiftMats * 32, 0);
+        crc_tables_host(slice.data(), h_crc_shift.data());
+        d_crc_slice = dmalloc<uint32_t>(slice.size(), n);
+        d_crc_shift = dmalloc<uint32_t>(h_crc_shift.size(), n);
+        upload(d_crc_slice, slice, stream);
+        upload(d_crc_shift, h_crc_shift, stream);
+        const auto tpl = image_template();
+        img_tpl_len = tpl.size();
+        img_frame_len = img_tpl_len + 4 * z.n_dirs * z.bins + 4;
+        img_frame_stride = (img_frame_len + 15) & ~uint64_t(15);
+        d_img_tpl = dmalloc<uint8_t>(tpl.size(), n);
+        upload(d_img_tpl, tpl, stream);
+        in_frame_len = 36 + 38 + packed_bytes + 4;
+        in_frame_stride = (in_frame_len + 15) & ~uint64_t(15);
+        const uint64_t B = max_batch;
+        d_frames_out = dmalloc<uint8_t>(B * img_frame_stride, n);
+        d_frames_in = dmalloc<uint8_t>(B * in_frame_stride, n);
+        d_ids = dmalloc<FrameIds>(B, n);
+        d_crc_acc = dmalloc<uint32_t>(2 * B, n);
+        d_crc_ok = dmalloc<int32_t>(B, n);
+        ck(cudaMallocHost(&h_frames_out, B * img_frame_len), "cudaMallocHost");
+        ck(cudaMallocHost(&h_frames_in, B * in_frame_len), "cudaMallocHost");
+        ck(cudaMallocHost(&h_ids, B * sizeof(FrameIds)), "cudaMallocHost");
+        ck(cudaMallocHost(&h_crc_ok, B * sizeof(int32_t)), "cudaMallocHost");
+    }
+    CrcTables crc_tables() const { return CrcTables{d_crc_slice, d_crc_shift}; }
 
     // Tensor-core delay-and-sum setup (beamform_tc.cu): clusters of <= kTcM
     // consecutive slots cut greedily so that R_c (the largest per-channel
@@ -610,6 +689,137 @@ struct sn_workspace {
             if (!out_pinned) std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
             done += c;
         }
+    }
+
+    // wire::error_frame(serial, ts, seq, message) (wire.cpp:278-287)
+    static std::vector<uint8_t> error_frame(uint32_t serial, uint64_t ts, uint64_t seq, const std::string& msg) {
+        std::vector<uint8_t> f;
+        const uint32_t magic = 0x45525449u;
+        const uint16_t version = 1, type = 5;
+        const uint64_t plen = msg.size();
+        put(f, &magic, 4); put(f, &version, 2); put(f, &type, 2); put(f, &serial, 4);
+        put(f, &ts, 8); put(f, &seq, 8); put(f, &plen, 8);
+        put(f, msg.data(), msg.size());
+        const uint32_t crc = crc32_host(f.data(), f.size());
+        put(f, &crc, 4);
+        return f;
+    }
+
+    // Central-node processing of received frames (central_node.cpp:130-160,
+    // 238-270, 316-323): packet checks (wire.cpp:95-168) and payload decode
+    // (wire.cpp:196-223) on the host from the 74 header bytes; the CRC of
+    // every well-formed measurement frame on the GPU; the pipeline; the
+    // processed-image frames (AIMG + CRC) encoded on the GPU. Per frame:
+    //   SN_OK          image frame (image_frame(img, m.seq))
+    //   SN_ERR_DECODE  process() rejected the measurement: error frame
+    //   SN_ERR_IO      malformed / integrity error / not a measurement: discarded
+    void process_frames(const uint8_t* const* frames, const uint64_t* lens, uint64_t count, uint8_t* out,
+                        uint64_t slot, uint64_t* out_lens, int32_t* status) {
+        require_device();
+        DeviceGuard g(device);
+        const Sizes& z = plan.sz;
+        std::vector<uint64_t> batch;
+        batch.reserve(max_batch);
+        auto flush = [&]() {
+            if (batch.empty()) return;
+            const uint64_t c = batch.size();
+            for (uint64_t i = 0; i < c; ++i) {
+                std::memcpy(h_frames_in + i * in_frame_len, frames[batch[i]], in_frame_len);
+                const uint8_t* f = frames[batch[i]];
+                FrameIds id{};
+                std::memcpy(&id.serial, f + 36, 4);
+                std::memcpy(&id.ts, f + 40, 8);
+                std::memcpy(&id.seq, f + 48, 8);
+                h_ids[i] = id;
+            }
+            ck(cudaMemcpy2DAsync(d_frames_in, in_frame_stride, h_frames_in, in_frame_len, in_frame_len, c,
+                                 cudaMemcpyHostToDevice, stream), "H2D frames");
+            ck(cudaMemcpyAsync(d_ids, h_ids, c * sizeof(FrameIds), cudaMemcpyHostToDevice, stream), "H2D ids");
+            ck(cudaMemsetAsync(d_crc_acc, 0, 2 * max_batch * sizeof(uint32_t), stream), "memset");
+            const CrcTables ct = crc_tables();
+            const uint64_t nin = in_frame_len - 4;
+            launch_crc_partial(d_frames_in, in_frame_stride, nin, c, ct, d_crc_acc, stream);
+            launch_crc_finalize(d_crc_acc, crc_init_term(h_crc_shift.data(), nin), c, d_frames_in, in_frame_stride,
+                                nin, false, d_crc_ok, stream);
+            ck(cudaMemcpy2DAsync(d_packed, packed_bytes, d_frames_in + 74, in_frame_stride, packed_bytes, c,
+                                 cudaMemcpyDeviceToDevice, stream), "D2D packed");
+            enqueue(d_packed, c, d_energy, stream);
+            ImageFrameArgs ia{d_energy, d_img_tpl, d_ids, d_frames_out, d_crc_acc + max_batch, energy_per,
+                              img_tpl_len, img_frame_len, img_frame_stride};
+            launch_encode_image_frames(ia, c, ct, stream);
+            const uint64_t nout = img_frame_len - 4;
+            launch_crc_finalize(d_crc_acc + max_batch, crc_init_term(h_crc_shift.data(), nout), c, d_frames_out,
+                                img_frame_stride, nout, true, nullptr, stream);
+            ck(cudaGetLastError(), "frame kernels");
+            ck(cudaMemcpy2DAsync(h_frames_out, img_frame_len, d_frames_out, img_frame_stride, img_frame_len, c,
+                                 cudaMemcpyDeviceToHost, stream), "D2H frames");
+            ck(cudaMemcpyAsync(h_crc_ok, d_crc_ok, c * sizeof(int32_t), cudaMemcpyDeviceToHost, stream), "D2H ok");
+            ck(cudaStreamSynchronize(stream), "frames sync");
+            for (uint64_t i = 0; i < c; ++i) {
+                const uint64_t k = batch[i];
+                if (h_crc_ok[i]) {
+                    std::memcpy(out + k * slot, h_frames_out + i * img_frame_len, img_frame_len);
+                    out_lens[k] = img_frame_len;
+                    status[k] = SN_OK;
+                } else {
+                    out_lens[k] = 0; // integrity error: frame discarded (wire.cpp:141-145)
+                    status[k] = SN_ERR_IO;
+                }
+            }
+            batch.clear();
+        };
+        for (uint64_t k = 0; k < count; ++k) {
+            out_lens[k] = 0;
+            status[k] = SN_ERR_IO;
+            const uint8_t* f = frames[k];
+            const uint64_t len = lens[k];
+            if (!f || len < 40) continue;
+            uint32_t magic;
+            uint16_t version, type;
+            uint64_t plen;
+            std::memcpy(&magic, f, 4);
+            std::memcpy(&version, f + 4, 2);
+            std::memcpy(&type, f + 6, 2);
+            std::memcpy(&plen, f + 28, 8);
+            if (magic != 0x45525449u || plen > (uint64_t{1} << 32) || len != 40 + plen) continue;
+            if (len != in_frame_len) {
+                // not this configuration's measurement size: host CRC, then the
+                // reference's decisions (discard, or an error frame from process())
+                uint32_t stored;
+                std::memcpy(&stored, f + 36 + plen, 4);
+                if (stored != crc32_host(f, 36 + plen)) continue;
+            }
+            if (version != 1 || type != 1) continue; // framing error / not a measurement
+            if (plen < 38) continue;                 // decode_raw_measurement: truncated
+            sn_raw_measurement m{};
+            std::memcpy(&m.sensor_serial, f + 36, 4);
+            std::memcpy(&m.timestamp_us, f + 40, 8);
+            std::memcpy(&m.seq, f + 48, 8);
+            std::memcpy(&m.channels, f + 56, 2);
+            std::memcpy(&m.frames, f + 58, 8);
+            std::memcpy(&m.pdm_rate, f + 66, 8);
+            m.packed = f + 74;
+            m.packed_len = plen - 38;
+            if (m.channels == 0 || m.frames == 0 || m.frames % 8 != 0 ||
+                m.packed_len != (uint64_t)m.channels * m.frames / 8) {
+                continue; // decode_raw_measurement rejects: malformed, discarded
+            }
+            try {
+                validate(m);
+            } catch (const Error& e) {
+                const auto ef = error_frame(m.sensor_serial, m.timestamp_us, m.seq, e.what());
+                if (ef.size() <= slot) {
+                    std::memcpy(out + k * slot, ef.data(), ef.size());
+                    out_lens[k] = ef.size();
+                }
+                status[k] = SN_ERR_DECODE;
+                continue;
+            }
+            batch.push_back(k);
+            if (batch.size() == max_batch) flush();
+        }
+        flush();
+        (void)z;
     }
 
     void process_device(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s) {
@@ -908,6 +1118,44 @@ sn_status sn_workspace_beamformer_info(const sn_workspace* ws, sn_beamformer_inf
         info->m = kTcM;
         info->n = kTcN;
         info->k = 32;
+    });
+}
+
+uint32_t sn_crc32(const uint8_t* bytes, uint64_t n) { return bytes || !n ? crc32_host(bytes, n) : 0; }
+
+uint64_t sn_workspace_image_frame_bytes(const sn_workspace* ws) { return ws ? ws->img_frame_len : 0; }
+
+sn_status sn_measurement_frame(const sn_raw_measurement* m, uint8_t* out, uint64_t capacity, uint64_t* n_out) {
+    return guarded([&] {
+        if (!m || (!m->packed && m->packed_len)) argument_error("null argument");
+        std::vector<uint8_t> f;
+        const uint32_t magic = 0x45525449u;
+        const uint16_t version = 1, type = 1;
+        const uint64_t plen = 38 + m->packed_len;
+        sn_workspace::put(f, &magic, 4); sn_workspace::put(f, &version, 2); sn_workspace::put(f, &type, 2);
+        sn_workspace::put(f, &m->sensor_serial, 4); sn_workspace::put(f, &m->timestamp_us, 8);
+        sn_workspace::put(f, &m->seq, 8); sn_workspace::put(f, &plen, 8);
+        sn_workspace::put(f, &m->sensor_serial, 4); sn_workspace::put(f, &m->timestamp_us, 8);
+        sn_workspace::put(f, &m->seq, 8); sn_workspace::put(f, &m->channels, 2);
+        sn_workspace::put(f, &m->frames, 8); sn_workspace::put(f, &m->pdm_rate, 8);
+        sn_workspace::put(f, m->packed, m->packed_len);
+        const uint32_t crc = crc32_host(f.data(), f.size());
+        sn_workspace::put(f, &crc, 4);
+        if (n_out) *n_out = f.size();
+        if (!out) return;
+        if (capacity < f.size()) argument_error("buffer too small");
+        std::memcpy(out, f.data(), f.size());
+    });
+}
+
+sn_status sn_workspace_process_frames(sn_workspace* ws, const uint8_t* const* frames, const uint64_t* lens,
+                                      uint64_t count, uint8_t* out, uint64_t slot_bytes, uint64_t* out_lens,
+                                      int32_t* status) {
+    return guarded([&] {
+        if (!ws || (count && (!frames || !lens || !out || !out_lens || !status))) argument_error("null argument");
+        ws->require_device();
+        if (slot_bytes < ws->img_frame_len) argument_error("output slot smaller than an image frame");
+        ws->process_frames(frames, lens, count, out, slot_bytes, out_lens, status);
     });
 }
 

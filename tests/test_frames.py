@@ -1,0 +1,105 @@
+"""Wire-format frames around the hot path: CRC-32
+(wire.cpp:58-63), the raw-measurement frame a sensor sends (wire.cpp:251-259)
+and the central node's frame processing (central_node.cpp:130-160, 238-270)
+with the processed-image frame (wire::image_frame(image_to_bytes(img), seq),
+wire.cpp:268-276, pipeline.cpp:109-125) encoded and CRC'd on the GPU.
+
+Oracle: the unmodified reference wire/pipeline code (oracle/_ref) and zlib's
+CRC-32 (same polynomial, init and xorout)."""
+import zlib
+
+import numpy as np
+import pytest
+
+from conftest import TINY, rel_rms, to_oracle
+
+
+def test_crc32_host_matches_zlib_and_reference(sn, ref):
+    rng = np.random.default_rng(1)
+    for n in [0, 1, 3, 4, 5, 255, 4096, 100003]:
+        d = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+        assert sn.crc32(d) == zlib.crc32(d) == ref.crc32(d)
+    assert sn.crc32(b"123456789") == 0xCBF43926  # CRC-32 check value
+
+
+def test_measurement_frame_bytes_match_reference(sn, po, ref):
+    cfg = sn.default_pipeline_config(sn.GridKind.horizontal90).copy(**TINY)
+    m = sn.synthesize_measurement(cfg, sn.Scene([sn.Reflector(0.7, 0.1, 0.0, 0.9)], 0.01, 3), 5, 1234, 17)
+    ours = sn.measurement_frame(m)
+    theirs = ref.measurement_frame(m.packed, m.frames, m.pdm_rate, m.sensor_serial, m.timestamp_us, m.seq)
+    assert ours == theirs
+    assert zlib.crc32(ours[:-4]) == int.from_bytes(ours[-4:], "little")
+
+
+# ---------------------------------------------------------------------------
+def _frame_parts(frame: bytes, n_dirs: int, bins: int):
+    E = 36 + 34 + 8 * n_dirs
+    head = frame[:E]
+    energies = np.frombuffer(frame[E:E + 4 * n_dirs * bins], np.float32).reshape(n_dirs, bins)
+    return head, energies
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["tiny", "h90", "hemi3000"])
+def test_process_frames_vs_reference_central_node(sn, po, ref, name):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    base = sn.default_pipeline_config(sn.GridKind.horizontal90)
+    cfg = {"tiny": base.copy(**TINY), "h90": base,
+           "hemi3000": sn.default_pipeline_config(sn.GridKind.hemisphere3000)}[name]
+    ws = sn.Workspace(cfg, device=0, max_batch=3)
+    rws = ref.workspace(to_oracle(po, cfg))
+    ms = [sn.synthesize_measurement(cfg, sn.Scene([sn.Reflector(0.6 + 0.2 * i, 0.3 - 0.2 * i, 0.0, 0.8)], 0.01, 40 + i),
+                                    serial=2 + i, timestamp_us=1000 * i + 7, seq=11 + i) for i in range(5)]
+    frames = [sn.measurement_frame(m) for m in ms]
+    got = ws.process_frames(frames)  # 5 frames through a 3-capture workspace: 3 + 2
+    nd, nb = ws.n_dirs, ws.bins
+    for (st, f), fin in zip(got, frames):
+        want = rws.process_frame(fin)
+        assert st == 0 and len(f) == len(want) == ws.image_frame_bytes
+        assert zlib.crc32(f[:-4]) == int.from_bytes(f[-4:], "little")     # our CRC (GPU) is the frame's CRC
+        h_got, e_got = _frame_parts(f, nd, nb)
+        h_want, e_want = _frame_parts(want, nd, nb)
+        assert h_got == h_want                                              # headers + direction table
+        w32 = e_want.astype(np.float32)
+        tol = np.spacing(np.abs(w32)).astype(np.float64) + 1e-12 * float(e_want.max())
+        assert (np.abs(e_got.astype(np.float64) - e_want) <= tol).all()
+        if np.array_equal(e_got, e_want):
+            assert f == want                                                # byte-identical frame
+
+
+@pytest.mark.gpu
+def test_process_frames_errors_like_the_central_node(sn, po, ref):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = sn.default_pipeline_config(sn.GridKind.horizontal90).copy(**TINY)
+    ws = sn.Workspace(cfg, device=0, max_batch=2)
+    rws = ref.workspace(to_oracle(po, cfg))
+    m = sn.synthesize_measurement(cfg, sn.Scene([sn.Reflector(0.7, 0.1, 0.0, 0.9)], 0.01, 3), 5, 1234, 17)
+    good = sn.measurement_frame(m)
+    # CRC mismatch: discarded (wire.cpp:141-145)
+    bad_crc = bytearray(good)
+    bad_crc[1000] ^= 0x10
+    # wrong pdm rate in a well-formed frame: process() throws -> error frame
+    m2 = sn.RawMeasurement(m.sensor_serial, m.timestamp_us, m.seq + 1, 32, m.frames, m.pdm_rate * 1.01, m.packed)
+    wrong_rate = sn.measurement_frame(m2)
+    # a frame of another configuration (more frames): error frame too
+    m3 = sn.RawMeasurement(7, 9, 3, 32, m.frames + 8, m.pdm_rate, np.zeros(4 * (m.frames + 8), np.uint8))
+    other_cfg = sn.measurement_frame(m3)
+    # garbage / truncated / not a measurement: discarded
+    trunc = good[:100]
+    got = ws.process_frames([good, bytes(bad_crc), wrong_rate, other_cfg, trunc, b"\0" * 64, good])
+    st = [s for s, _ in got]
+    assert st == [0, 4, 3, 3, 4, 4, 0]  # ok, discarded, error frame x2, discarded x2, ok
+    assert got[0][1] == got[6][1] and got[1][1] == b"" and got[4][1] == b""
+    for k, mm in ((2, m2), (3, m3)):
+        f = got[k][1]
+        assert zlib.crc32(f[:-4]) == int.from_bytes(f[-4:], "little")
+        assert int.from_bytes(f[6:8], "little") == 5                      # MsgType::error
+        with pytest.raises(po.OracleError) as e:
+            rws.process_frame(wrong_rate if k == 2 else other_cfg)
+        assert f[36:-4].decode() == e.value.msg                           # the reference's message
+    with pytest.raises(po.OracleError):
+        rws.process_frame(bytes(bad_crc))
