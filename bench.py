@@ -325,6 +325,44 @@ def run_b200(args):
         e2e_s = float(t.item())
     e2e_value = world * e2e_steps * B / e2e_s
 
+    # ---- wire path: raw-measurement frames in, processed-image frames out ------
+    # (the central node's traffic: CRC-checked on the GPU, AIMG frames encoded
+    # and CRC'd on the GPU; sn_workspace_process_frames; pinned host buffers)
+    import ctypes as C
+    L = sn.lib()
+    slot = ws.image_frame_bytes
+    fr = [sn.measurement_frame(sn.RawMeasurement(serial, k, k, 32, ws.frames, cfg.pdm_rate, pool_h[k]))
+          for k in range(2 * B)]
+    flen = len(fr[0])
+    fin = torch.empty((2 * B, flen), dtype=torch.uint8).pin_memory()
+    fin_np = fin.numpy()
+    for k in range(2 * B):
+        fin_np[k] = np.frombuffer(fr[k], np.uint8)
+    fout = torch.empty((B, slot), dtype=torch.uint8).pin_memory()
+    ptrs = [(C.c_void_p * B)(*[fin_np[h * B + i].ctypes.data for i in range(B)]) for h in range(2)]
+    lens = (C.c_uint64 * B)(*([flen] * B))
+    olen, ost = (C.c_uint64 * B)(), (C.c_int32 * B)()
+    fout_ptr = fout.numpy().ctypes.data
+
+    def wire_step(k):
+        rc = L.sn_workspace_process_frames(ws._h, ptrs[k % 2], lens, B, fout_ptr, slot, olen, ost)
+        if rc != 0 or any(ost[i] != 0 for i in range(B)):
+            raise RuntimeError(f"process_frames failed: rc={rc} status={list(ost)}")
+
+    for k in range(max(1, args.warmup)):
+        wire_step(k)
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        wire_step(k)
+    wire_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([wire_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wire_s = float(t.item())
+    wire_value = world * e2e_steps * B / wire_s
+
     # ---- single-capture latency (host API, 1 capture) -------------------------
     lat = []
     m = sn.RawMeasurement(serial, 0, 0, 32, ws.frames, cfg.pdm_rate, pool_h[0])
@@ -398,6 +436,10 @@ def run_b200(args):
                 "h2d_bytes_per_step": B * 32 * d["frames"] // 8,
                 "d2h_bytes_per_step": B * 4 * d["n_directions"] * d["range_bins"],
                 "api": "Workspace.process_packed_host (sn_workspace_process_batch), pinned buffers"},
+        "e2e_wire": {"value": wire_value, "unit": UNIT, "h2d_bytes_per_step": B * flen,
+                     "d2h_bytes_per_step": B * slot,
+                     "api": "sn_workspace_process_frames: raw-measurement frames in (CRC verified on the GPU), "
+                            "processed-image frames out (AIMG encoded + CRC on the GPU), pinned buffers"},
         "latency_ms": {
             "p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
             "device_p50": float(np.percentile(dev_lat, 50)),

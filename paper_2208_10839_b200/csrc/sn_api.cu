@@ -718,22 +718,28 @@ struct sn_workspace {
         require_device();
         DeviceGuard g(device);
         const Sizes& z = plan.sz;
+        const bool out_pinned = is_pinned(out);
         std::vector<uint64_t> batch;
         batch.reserve(max_batch);
         auto flush = [&]() {
             if (batch.empty()) return;
             const uint64_t c = batch.size();
             for (uint64_t i = 0; i < c; ++i) {
-                std::memcpy(h_frames_in + i * in_frame_len, frames[batch[i]], in_frame_len);
                 const uint8_t* f = frames[batch[i]];
+                if (is_pinned(f)) {
+                    ck(cudaMemcpyAsync(d_frames_in + i * in_frame_stride, f, in_frame_len, cudaMemcpyHostToDevice,
+                                       stream), "H2D frame");
+                } else {
+                    std::memcpy(h_frames_in + i * in_frame_len, f, in_frame_len);
+                    ck(cudaMemcpyAsync(d_frames_in + i * in_frame_stride, h_frames_in + i * in_frame_len,
+                                       in_frame_len, cudaMemcpyHostToDevice, stream), "H2D frame");
+                }
                 FrameIds id{};
                 std::memcpy(&id.serial, f + 36, 4);
                 std::memcpy(&id.ts, f + 40, 8);
                 std::memcpy(&id.seq, f + 48, 8);
                 h_ids[i] = id;
             }
-            ck(cudaMemcpy2DAsync(d_frames_in, in_frame_stride, h_frames_in, in_frame_len, in_frame_len, c,
-                                 cudaMemcpyHostToDevice, stream), "H2D frames");
             ck(cudaMemcpyAsync(d_ids, h_ids, c * sizeof(FrameIds), cudaMemcpyHostToDevice, stream), "H2D ids");
             ck(cudaMemsetAsync(d_crc_acc, 0, 2 * max_batch * sizeof(uint32_t), stream), "memset");
             const CrcTables ct = crc_tables();
@@ -751,14 +757,22 @@ struct sn_workspace {
             launch_crc_finalize(d_crc_acc + max_batch, crc_init_term(h_crc_shift.data(), nout), c, d_frames_out,
                                 img_frame_stride, nout, true, nullptr, stream);
             ck(cudaGetLastError(), "frame kernels");
-            ck(cudaMemcpy2DAsync(h_frames_out, img_frame_len, d_frames_out, img_frame_stride, img_frame_len, c,
-                                 cudaMemcpyDeviceToHost, stream), "D2H frames");
+            // D2H straight into the caller's slots when they are page-locked
+            // (consecutive batch entries are consecutive slots in the common case)
+            const bool direct = out_pinned && batch.back() - batch.front() == c - 1;
+            if (direct) {
+                ck(cudaMemcpy2DAsync(out + batch.front() * slot, slot, d_frames_out, img_frame_stride, img_frame_len, c,
+                                     cudaMemcpyDeviceToHost, stream), "D2H frames");
+            } else {
+                ck(cudaMemcpy2DAsync(h_frames_out, img_frame_len, d_frames_out, img_frame_stride, img_frame_len, c,
+                                     cudaMemcpyDeviceToHost, stream), "D2H frames");
+            }
             ck(cudaMemcpyAsync(h_crc_ok, d_crc_ok, c * sizeof(int32_t), cudaMemcpyDeviceToHost, stream), "D2H ok");
             ck(cudaStreamSynchronize(stream), "frames sync");
             for (uint64_t i = 0; i < c; ++i) {
                 const uint64_t k = batch[i];
                 if (h_crc_ok[i]) {
-                    std::memcpy(out + k * slot, h_frames_out + i * img_frame_len, img_frame_len);
+                    if (!direct) std::memcpy(out + k * slot, h_frames_out + i * img_frame_len, img_frame_len);
                     out_lens[k] = img_frame_len;
                     status[k] = SN_OK;
                 } else {
