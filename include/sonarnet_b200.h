@@ -42,7 +42,8 @@ typedef enum sn_status {
     SN_ERR_DECODE = 3,
     SN_ERR_IO = 4,
     SN_ERR_CUDA = 5,
-    SN_ERR_INTERNAL = 6
+    SN_ERR_INTERNAL = 6,
+    SN_ERR_NOT_READY = 7   /* sn_pool_poll: nothing released within the timeout */
 } sn_status;
 
 /* geometry.hpp:65 GridKind */
@@ -264,6 +265,28 @@ uint64_t sn_workspace_image_frame_bytes(const sn_workspace* ws);
 sn_status sn_workspace_process_frames(sn_workspace* ws, const uint8_t* const* frames, const uint64_t* lens,
                                       uint64_t count, uint8_t* out, uint64_t slot_bytes, uint64_t* out_lens,
                                       int32_t* status);
+
+/* ---- GPU-backed central-node worker pool (central_node.cpp:48-53, 130-160,
+ * 224-336) ----------------------------------------------------------------
+ * K = n_devices x workers_per_device workers, each owning a Workspace; frames
+ * are ticketed per sensor at submission, processed in device batches of up to
+ * max_batch (sn_workspace_process_frames), and released strictly in per-sensor
+ * submission order. submit blocks while the input queue is full (backpressure)
+ * and returns SN_ERR_IO for a frame the ingest would drop (bad magic, length,
+ * version or type). poll returns the next released result: status SN_OK with
+ * the processed-image frame, SN_ERR_DECODE with the reference's error frame,
+ * SN_ERR_IO (CRC mismatch, discarded) with no bytes; out == NULL peeks at the
+ * length without consuming. */
+typedef struct sn_pool sn_pool;
+sn_status sn_pool_create(const sn_pipeline_config* cfg, const int* devices, int n_devices,
+                         int workers_per_device, uint64_t max_batch, sn_pool** out);
+void sn_pool_destroy(sn_pool* pool);
+sn_status sn_pool_submit(sn_pool* pool, const uint8_t* frame, uint64_t len);
+sn_status sn_pool_poll(sn_pool* pool, int timeout_ms, uint8_t* out, uint64_t capacity, uint64_t* len,
+                       int32_t* status, uint32_t* serial, uint64_t* seq);
+/* stats: submitted, completed, discarded (CRC), workers */
+sn_status sn_pool_stats(sn_pool* pool, uint64_t* stats4);
+uint64_t sn_pool_frame_bytes(const sn_pool* pool);
 
 /* FMA-throughput microbenchmark on `device` (TFLOP/s, FMA = 2 flops); the
  * roofline denominator for CUDA-core kernels (no tensor cores involved). */

@@ -33,7 +33,7 @@ __all__ = [
     "GridKind", "Precision", "PipelineConfig", "RawMeasurement", "AcousticImage", "Reflector",
     "Scene", "Workspace", "default_pipeline_config", "direction_grid", "default_array",
     "synthesize_measurement", "SonarError", "ConfigError", "ArgumentError", "DecodeError",
-    "IoError", "CudaError", "lib", "crc32", "measurement_frame",
+    "IoError", "CudaError", "lib", "crc32", "measurement_frame", "CentralPool",
 ]
 
 
@@ -182,6 +182,14 @@ def lib() -> C.CDLL:
     L.sn_workspace_stage_times.argtypes = [vp, vp]
     L.sn_measure_fp_peak.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
     L.sn_workspace_beamformer_info.argtypes = [vp, C.POINTER(_BfInfo)]
+    L.sn_pool_create.argtypes = [C.POINTER(_Config), C.POINTER(C.c_int), C.c_int, C.c_int, u64, C.POINTER(vp)]
+    L.sn_pool_destroy.argtypes = [vp]
+    L.sn_pool_submit.argtypes = [vp, vp, u64]
+    L.sn_pool_poll.argtypes = [vp, C.c_int, vp, u64, C.POINTER(u64), C.POINTER(C.c_int32),
+                               C.POINTER(C.c_uint32), C.POINTER(u64)]
+    L.sn_pool_stats.argtypes = [vp, C.POINTER(u64)]
+    L.sn_pool_frame_bytes.restype = u64
+    L.sn_pool_frame_bytes.argtypes = [vp]
     L.sn_crc32.restype = C.c_uint32
     L.sn_crc32.argtypes = [vp, u64]
     L.sn_measurement_frame.argtypes = [C.POINTER(_Measurement), vp, u64, C.POINTER(u64)]
@@ -207,6 +215,60 @@ def measure_fp_peak(device: int = 0, precision: Precision = Precision.f64) -> fl
 
 
 # ---------------------------------------------------------------------------
+class CentralPool:
+    """GPU-backed central-node worker pool (sn_pool_*; central_node.cpp:48-53,
+    130-160, 224-336): K workers with one Workspace each, per-sensor FIFO release.
+
+        pool = CentralPool(cfg, devices=[0], workers_per_device=2, max_batch=8)
+        pool.submit(frame)                  # raw-measurement frame (wire bytes)
+        serial, seq, status, frame = pool.poll(timeout_ms=1000)
+    """
+
+    def __init__(self, cfg: PipelineConfig, devices=(0,), workers_per_device: int = 1, max_batch: int = 1):
+        st, self._keep = cfg._struct()
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(lib().sn_pool_create(C.byref(st), devs, len(devices), workers_per_device, max_batch, C.byref(h)))
+        self._h = h
+        self.frame_bytes = int(lib().sn_pool_frame_bytes(self._h))
+        self._buf = np.empty(self.frame_bytes, np.uint8)
+
+    def submit(self, frame: bytes) -> bool:
+        """False when the ingest would drop the frame (bad magic/length/type)."""
+        b = np.frombuffer(frame, np.uint8)
+        rc = lib().sn_pool_submit(self._h, b.ctypes.data, b.size)
+        if rc == IoError.status:
+            return False
+        _check(rc)
+        return True
+
+    def poll(self, timeout_ms: int = -1):
+        """Next released result (serial, seq, status, frame_bytes), or None on timeout."""
+        n, st, ser, seq = C.c_uint64(0), C.c_int32(0), C.c_uint32(0), C.c_uint64(0)
+        rc = lib().sn_pool_poll(self._h, timeout_ms, self._buf.ctypes.data, self._buf.size, C.byref(n),
+                                C.byref(st), C.byref(ser), C.byref(seq))
+        if rc == 7:  # SN_ERR_NOT_READY
+            return None
+        _check(rc)
+        return int(ser.value), int(seq.value), int(st.value), self._buf[:n.value].tobytes()
+
+    def stats(self) -> dict:
+        s = (C.c_uint64 * 4)()
+        _check(lib().sn_pool_stats(self._h, s))
+        return {"submitted": s[0], "completed": s[1], "discarded": s[2], "workers": s[3]}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sn_pool_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def crc32(data) -> int:
     """wire::crc32 (wire.cpp:58-63), host implementation of the C ABI."""
     b = np.ascontiguousarray(np.frombuffer(bytes(data), np.uint8))

@@ -862,6 +862,7 @@ const char* sn_status_name(sn_status s) {
         case SN_ERR_DECODE: return "decode";
         case SN_ERR_IO: return "io";
         case SN_ERR_CUDA: return "cuda";
+        case SN_ERR_NOT_READY: return "not ready";
         default: return "internal";
     }
 }

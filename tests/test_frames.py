@@ -103,3 +103,61 @@ def test_process_frames_errors_like_the_central_node(sn, po, ref):
         assert f[36:-4].decode() == e.value.msg                           # the reference's message
     with pytest.raises(po.OracleError):
         rws.process_frame(bytes(bad_crc))
+
+
+# ---------------------------------------------------------------------------
+# GPU-backed central-node worker pool: per-sensor FIFO
+# release and K-transparency (test_nodes.cpp:396-445: K=1 and K=8 workers give
+# identical bytes per sensor)
+def _pool_run(sn, cfg, frames, workers, max_batch):
+    pool = sn.CentralPool(cfg, devices=[0], workers_per_device=workers, max_batch=max_batch)
+    accepted = sum(pool.submit(f) for f in frames)
+    out = [pool.poll(timeout_ms=60000) for _ in range(accepted)]
+    stats = pool.stats()
+    pool.close()
+    return accepted, out, stats
+
+
+@pytest.mark.gpu
+def test_central_pool_fifo_and_worker_transparency(sn, po, ref):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = sn.default_pipeline_config(sn.GridKind.horizontal90).copy(**TINY)
+    frames, meta = [], []
+    for k in range(6):
+        for serial in (3, 9, 4):
+            m = sn.synthesize_measurement(cfg, sn.Scene([sn.Reflector(0.5 + 0.05 * k, 0.1 * serial - 0.5, 0.0, 0.8)],
+                                                        0.01, 100 * serial + k), serial=serial,
+                                          timestamp_us=1000 * k, seq=k)
+            frames.append(sn.measurement_frame(m))
+            meta.append((serial, k))
+    bad = bytearray(frames[4])          # sensor 9, seq 1: CRC mismatch -> discarded in order
+    bad[500] ^= 1
+    frames[4] = bytes(bad)
+    frames.insert(7, b"garbage" * 20)   # dropped at ingest: no ticket
+    rws = ref.workspace(to_oracle(po, cfg))
+    results = {}
+    for workers, mb in ((1, 1), (3, 2)):
+        accepted, out, stats = _pool_run(sn, cfg, frames, workers, mb)
+        assert accepted == 18 and stats["completed"] == 18 and stats["discarded"] == 1
+        per = {}
+        for serial, seq, status, f in out:
+            per.setdefault(serial, []).append((seq, status, f))
+        for serial, lst in per.items():
+            assert [s for s, _, _ in lst] == list(range(6))          # per-sensor FIFO
+        results[workers] = per
+    assert results[1] == results[3]                                    # K-transparent
+    # against the reference central node's frames
+    fi = 0
+    for f in frames:
+        if f.startswith(b"garbage"):
+            continue
+        serial, k = meta[fi]
+        fi += 1
+        seq, status, got = results[3][serial][k]
+        if serial == 9 and k == 1:
+            assert status == 4 and got == b""
+            continue
+        want = rws.process_frame(f)
+        assert status == 0 and len(got) == len(want) and got[:36] == want[:36]
