@@ -284,6 +284,10 @@ void sn_pool_destroy(sn_pool* pool);
 sn_status sn_pool_submit(sn_pool* pool, const uint8_t* frame, uint64_t len);
 sn_status sn_pool_poll(sn_pool* pool, int timeout_ms, uint8_t* out, uint64_t capacity, uint64_t* len,
                        int32_t* status, uint32_t* serial, uint64_t* seq);
+/* Zero-copy variant: *data points at the released frame inside the pool's
+ * page-locked result block, valid until the next sn_pool_poll_view call. */
+sn_status sn_pool_poll_view(sn_pool* pool, int timeout_ms, const uint8_t** data, uint64_t* len, int32_t* status,
+                            uint32_t* serial, uint64_t* seq);
 /* stats: submitted, completed, discarded (CRC), workers */
 sn_status sn_pool_stats(sn_pool* pool, uint64_t* stats4);
 uint64_t sn_pool_frame_bytes(const sn_pool* pool);

@@ -188,6 +188,8 @@ def lib() -> C.CDLL:
     L.sn_pool_poll.argtypes = [vp, C.c_int, vp, u64, C.POINTER(u64), C.POINTER(C.c_int32),
                                C.POINTER(C.c_uint32), C.POINTER(u64)]
     L.sn_pool_stats.argtypes = [vp, C.POINTER(u64)]
+    L.sn_pool_poll_view.argtypes = [vp, C.c_int, C.POINTER(C.c_void_p), C.POINTER(u64), C.POINTER(C.c_int32),
+                                    C.POINTER(C.c_uint32), C.POINTER(u64)]
     L.sn_pool_frame_bytes.restype = u64
     L.sn_pool_frame_bytes.argtypes = [vp]
     L.sn_crc32.restype = C.c_uint32

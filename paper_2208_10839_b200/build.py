@@ -25,6 +25,7 @@ INCLUDE = os.path.join(ROOT, "include")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
+CUDA_INC = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(NVCC))), "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 HOST_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
@@ -60,7 +61,7 @@ def build(verbose: bool = False) -> str:
             s = os.path.join(CSRC, src)
             o = os.path.join(OBJ, src + ".o")
             if _newer(o, [s] + hdr + [__file__]):
-                _run([CXX, *HOST_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o], log)
+                _run([CXX, *HOST_FLAGS, "-I", INCLUDE, "-I", CSRC, "-I", CUDA_INC, "-c", s, "-o", o], log)
             objs.append(o)
         for src in CU_SOURCES:
             s = os.path.join(CSRC, src)

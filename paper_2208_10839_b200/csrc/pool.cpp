@@ -15,6 +15,8 @@
 // are not held back.
 #include "sonarnet_b200.h"
 
+#include <cuda_runtime.h>
+
 #include <algorithm>
 #include <chrono>
 #include <condition_variable>
@@ -36,11 +38,30 @@ struct Item {
     std::vector<uint8_t> frame;
 };
 
+// Page-locked result block of one worker batch (max_batch slots): the GPU
+// writes the image frames straight into it; outcomes reference their slot and
+// the block returns to its worker's free list when the last one is polled.
+struct Block {
+    uint8_t* data = nullptr;
+    std::mutex* m = nullptr;
+    std::vector<uint8_t*>* free_list = nullptr;
+};
+struct BlockRelease {
+    void operator()(Block* b) const {
+        {
+            std::lock_guard<std::mutex> lk(*b->m);
+            b->free_list->push_back(b->data);
+        }
+        delete b;
+    }
+};
+
 struct Outcome {
     uint32_t serial = 0;
     uint64_t seq = 0;
     int32_t status = SN_OK;
-    std::vector<uint8_t> bytes;
+    std::shared_ptr<Block> block; // frame bytes at block->data + offset
+    uint64_t offset = 0, len = 0;
 };
 
 } // namespace
@@ -56,9 +77,29 @@ struct sn_pool {
     std::map<uint32_t, uint64_t> next_ticket, next_release;
     std::map<std::pair<uint32_t, uint64_t>, Outcome> pending;
     std::deque<Outcome> released;
+    Outcome view; // result handed out by sn_pool_poll_view, valid until the next call
     bool closing = false;
     uint64_t submitted = 0, completed = 0, discarded = 0;
     std::string worker_error;
+    std::mutex blocks_m;
+    std::vector<uint8_t*> free_blocks, all_blocks;
+    uint64_t block_bytes = 0;
+
+    uint8_t* take_block() {
+        {
+            std::lock_guard<std::mutex> lk(blocks_m);
+            if (!free_blocks.empty()) {
+                uint8_t* b = free_blocks.back();
+                free_blocks.pop_back();
+                return b;
+            }
+        }
+        uint8_t* b = nullptr;
+        if (cudaMallocHost(&b, block_bytes) != cudaSuccess) return nullptr;
+        std::lock_guard<std::mutex> lk(blocks_m);
+        all_blocks.push_back(b);
+        return b;
+    }
 
     ~sn_pool() {
         {
@@ -70,7 +111,11 @@ struct sn_pool {
         for (auto& t : workers) {
             if (t.joinable()) t.join();
         }
+        pending.clear();
+        released.clear();
+        view = Outcome{};
         for (auto* w : workspaces) sn_workspace_destroy(w);
+        for (uint8_t* b : all_blocks) cudaFreeHost(b);
     }
 
     // move every outcome whose ticket is next for its sensor to `released`
@@ -95,7 +140,6 @@ struct sn_pool {
     void worker_loop(size_t index) {
         sn_workspace* ws = workspaces[index];
         const uint64_t slot = sn_workspace_image_frame_bytes(ws);
-        std::vector<uint8_t> out(max_batch * slot);
         std::vector<uint64_t> out_lens(max_batch);
         std::vector<int32_t> status(max_batch);
         std::vector<const uint8_t*> ptrs(max_batch);
@@ -116,8 +160,14 @@ struct sn_pool {
                 ptrs[i] = batch[i].frame.data();
                 lens[i] = batch[i].frame.size();
             }
-            const sn_status rc = sn_workspace_process_frames(ws, ptrs.data(), lens.data(), batch.size(), out.data(),
-                                                             slot, out_lens.data(), status.data());
+            uint8_t* raw = take_block();
+            sn_status rc = SN_ERR_CUDA;
+            std::shared_ptr<Block> block;
+            if (raw) {
+                block.reset(new Block{raw, &blocks_m, &free_blocks}, BlockRelease{});
+                rc = sn_workspace_process_frames(ws, ptrs.data(), lens.data(), batch.size(), raw, slot,
+                                                 out_lens.data(), status.data());
+            }
             std::vector<Outcome> outs(batch.size());
             for (size_t i = 0; i < batch.size(); ++i) {
                 Outcome& o = outs[i];
@@ -127,7 +177,9 @@ struct sn_pool {
                     o.status = rc;
                 } else {
                     o.status = status[i];
-                    o.bytes.assign(out.data() + i * slot, out.data() + i * slot + out_lens[i]);
+                    o.block = block;
+                    o.offset = i * slot;
+                    o.len = out_lens[i];
                 }
             }
             {
@@ -136,7 +188,7 @@ struct sn_pool {
                 // bounded reorder window (central_node.cpp:224-236): wait while it
                 // is full unless one of ours is the next to be released
                 cv_space.wait(lk, [&] {
-                    if (closing || pending.size() + outs.size() <= window_capacity) return true;
+                    if (closing || pending.size() + released.size() + outs.size() <= window_capacity) return true;
                     for (size_t i = 0; i < batch.size(); ++i)
                         if (next_release[batch[i].serial] == batch[i].ticket) return true;
                     return false;
@@ -172,8 +224,19 @@ sn_status sn_pool_create(const sn_pipeline_config* cfg, const int* devices, int 
         }
     }
     const size_t k = pool->workspaces.size();
+    pool->block_bytes = pool->max_batch * sn_workspace_image_frame_bytes(pool->workspaces[0]);
     pool->input_capacity = 4 * k * pool->max_batch;
-    pool->window_capacity = 4 * k * pool->max_batch;
+    pool->window_capacity = 2 * k * pool->max_batch;
+    // result blocks for the steady state: one in flight per worker, the
+    // bounded window's worth, one being viewed (allocated up front: page-locked
+    // allocations are slow)
+    const size_t nblocks = 2 * k + pool->window_capacity / pool->max_batch + 1;
+    for (size_t i = 0; i < nblocks; ++i) {
+        uint8_t* b = nullptr;
+        if (cudaMallocHost(&b, pool->block_bytes) != cudaSuccess) return SN_ERR_CUDA;
+        pool->all_blocks.push_back(b);
+        pool->free_blocks.push_back(b);
+    }
     for (size_t i = 0; i < k; ++i) {
         sn_pool* p = pool.get();
         pool->workers.emplace_back([p, i] { p->worker_loop(i); });
@@ -224,15 +287,45 @@ sn_status sn_pool_poll(sn_pool* pool, int timeout_ms, uint8_t* out, uint64_t cap
         return SN_ERR_NOT_READY;
     }
     Outcome& o = pool->released.front();
-    *len = o.bytes.size();
+    *len = o.len;
     *status = o.status;
     if (serial) *serial = o.serial;
     if (seq) *seq = o.seq;
     if (!out) return SN_OK; // peek
-    if (capacity < o.bytes.size()) return SN_ERR_ARGUMENT;
-    std::memcpy(out, o.bytes.data(), o.bytes.size());
+    if (capacity < o.len) return SN_ERR_ARGUMENT;
+    Outcome taken = std::move(o);
     pool->released.pop_front();
+    lk.unlock(); // copy outside the lock; the block stays alive through `taken`
+    pool->cv_space.notify_all();
+    if (taken.len) std::memcpy(out, taken.block->data + taken.offset, taken.len);
     return SN_OK;
+}
+
+sn_status sn_pool_poll_view(sn_pool* pool, int timeout_ms, const uint8_t** data, uint64_t* len, int32_t* status,
+                            uint32_t* serial, uint64_t* seq) {
+    if (!pool || !data || !len || !status) return SN_ERR_ARGUMENT;
+    Outcome old;
+    {
+        std::unique_lock<std::mutex> lk(pool->m);
+        auto ready = [&] { return !pool->released.empty(); };
+        if (timeout_ms < 0) pool->cv_out.wait(lk, ready);
+        else if (!pool->cv_out.wait_for(lk, std::chrono::milliseconds(timeout_ms), ready)) {
+            *len = 0;
+            *data = nullptr;
+            return SN_ERR_NOT_READY;
+        }
+        old = std::move(pool->view);
+        pool->view = std::move(pool->released.front());
+        pool->released.pop_front();
+        const Outcome& o = pool->view;
+        *data = o.len ? o.block->data + o.offset : nullptr;
+        *len = o.len;
+        *status = o.status;
+        if (serial) *serial = o.serial;
+        if (seq) *seq = o.seq;
+    }
+    pool->cv_space.notify_all();
+    return SN_OK; // `old` (the previous view) is released here, outside the lock
 }
 
 sn_status sn_pool_stats(sn_pool* pool, uint64_t* stats4) {
