@@ -7,6 +7,9 @@
 #ifndef SNB_ENV_MINB
 #define SNB_ENV_MINB 2 // envelope CTAs per SM the register budget is sized for
 #endif
+#ifndef SNB_ENV_MINB_F32
+#define SNB_ENV_MINB_F32 2
+#endif
 #include <type_traits>
 
 namespace snb {
@@ -387,7 +390,8 @@ __device__ __forceinline__ void fir_polyphase(const R* ph, const R* comp, const 
 }
 
 template <typename R, int G, int M>
-__global__ void __launch_bounds__(kThreads * G, SNB_ENV_MINB / G) k_envelope(EnvArgs a, FirTaps<R> taps) {
+__global__ void __launch_bounds__(kThreads * G, (sizeof(R) == 8 ? SNB_ENV_MINB : SNB_ENV_MINB_F32) / G)
+    k_envelope(EnvArgs a, FirTaps<R> taps) {
     using V = typename Cx<R>::T;
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int N = 2 * M;
@@ -424,6 +428,17 @@ __global__ void __launch_bounds__(kThreads * G, SNB_ENV_MINB / G) k_envelope(Env
     for (int64_t it = (int64_t)blockIdx.x * G + grp; it < items; it += (int64_t)gridDim.x * G) {
         const int64_t b = it / a.n_dirs, slot = it % a.n_dirs;
         const R* src = reinterpret_cast<const R*>(a.beams) + (size_t)it * N;
+#ifndef SNB_NO_BEAM_PREFETCH
+        {
+            // pull the next item's beam (N reals) into L2 while this one runs
+            const int64_t nx = it + (int64_t)gridDim.x * G;
+            if (nx < items && tid == 0) {
+                const R* nsrc = reinterpret_cast<const R*>(a.beams) + (size_t)nx * N;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nsrc), "r"((unsigned)(N * sizeof(R)))
+                             : "memory");
+            }
+        }
+#endif
         cfft<M, false, false>(reinterpret_cast<const V*>(src), bufB, twsrc);
         real_spectral_op(bufB, M, twsrc, [&](V X, int k) {
             if (k == 0 || k == M) return V{(R)0, (R)0};
