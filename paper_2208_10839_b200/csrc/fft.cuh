@@ -168,72 +168,81 @@ template <typename V> struct TwShared {
     }
 };
 
-// One Stockham pass: radix RADIX, current sub-transform length ns.
+// One Stockham pass: radix RADIX, current sub-transform length ns, M points.
 // src element i at src[SRC_PADDED ? pad16(i) : i]; dst always padded.
 // In place (src == dst) is allowed: every thread loads all of its inputs
-// before a CTA barrier, then stores.
-template <int RADIX, bool INV, bool SRC_PADDED, typename V, typename TW>
-__device__ __forceinline__ void stockham_pass(const V* src, V* dst, int M, int ns, const TW& tw) {
-    const int nj = M / RADIX;
-    const int j = gtid();
-    V v[RADIX];
-    const bool active = j < nj;
-    if (active) {
+// before a CTA barrier, then stores. M / RADIX butterflies over kGroupThreads
+// threads: BPT = ceil(M / RADIX / kGroupThreads) per thread (1 up to M = 4096
+// with radix 16, 2 for M = 8192).
+template <int RADIX, bool INV, bool SRC_PADDED, int M, typename V, typename TW>
+__device__ __forceinline__ void stockham_pass(const V* src, V* dst, int ns, const TW& tw) {
+    constexpr int nj = M / RADIX;
+    constexpr int BPT = (nj + kGroupThreads - 1) / kGroupThreads;
+    V v[BPT][RADIX];
 #pragma unroll
-        for (int r = 0; r < RADIX; ++r) {
-            const int i = j + r * nj;
-            v[r] = src[SRC_PADDED ? pad16(i) : i];
-        }
-        const int k = j % ns;
-        if (ns > 1) {
-            if constexpr (RADIX == 16) {
-                // w^1, w^2, w^4, w^8 from the table, the other powers by at most
-                // three products (<= 3 roundings): 4 loads instead of 15
-                V w[16];
-                w[1] = tw.w(M, ns, 16, k, 1);
-                w[2] = tw.w(M, ns, 16, k, 2);
-                w[4] = tw.w(M, ns, 16, k, 4);
-                w[8] = tw.w(M, ns, 16, k, 8);
-                w[3] = cmul(w[1], w[2]);
-                w[5] = cmul(w[1], w[4]);
-                w[6] = cmul(w[2], w[4]);
-                w[7] = cmul(w[3], w[4]);
+    for (int bt = 0; bt < BPT; ++bt) {
+        const int j = gtid() + bt * kGroupThreads;
+        if (j < nj) {
 #pragma unroll
-                for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
+            for (int r = 0; r < RADIX; ++r) {
+                const int i = j + r * nj;
+                v[bt][r] = src[SRC_PADDED ? pad16(i) : i];
+            }
+            const int k = j % ns;
+            if (ns > 1) {
+                if constexpr (RADIX == 16) {
+                    // w^1, w^2, w^4, w^8 from the table, the other powers by at most
+                    // three products (<= 3 roundings): 4 loads instead of 15
+                    V w[16];
+                    w[1] = tw.w(M, ns, 16, k, 1);
+                    w[2] = tw.w(M, ns, 16, k, 2);
+                    w[4] = tw.w(M, ns, 16, k, 4);
+                    w[8] = tw.w(M, ns, 16, k, 8);
+                    w[3] = cmul(w[1], w[2]);
+                    w[5] = cmul(w[1], w[4]);
+                    w[6] = cmul(w[2], w[4]);
+                    w[7] = cmul(w[3], w[4]);
 #pragma unroll
-                for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], INV ? cconj(w[r]) : w[r]);
-            } else {
+                    for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
 #pragma unroll
-                for (int r = 1; r < RADIX; ++r) {
-                    V w = tw.w(M, ns, RADIX, k, r);
-                    if (INV) w.y = -w.y;
-                    v[r] = cmul(v[r], w);
+                    for (int r = 1; r < 16; ++r) v[bt][r] = cmul(v[bt][r], INV ? cconj(w[r]) : w[r]);
+                } else {
+#pragma unroll
+                    for (int r = 1; r < RADIX; ++r) {
+                        V w = tw.w(M, ns, RADIX, k, r);
+                        if (INV) w.y = -w.y;
+                        v[bt][r] = cmul(v[bt][r], w);
+                    }
                 }
             }
+            dft_r<RADIX, INV>(v[bt]);
         }
-        dft_r<RADIX, INV>(v);
     }
     gsync();
-    if (active) {
-        const int k = j % ns;
-        const int base = (j / ns) * ns * RADIX + k;
 #pragma unroll
-        for (int r = 0; r < RADIX; ++r) dst[pad16(base + out_slot<RADIX>(r) * ns)] = v[r];
+    for (int bt = 0; bt < BPT; ++bt) {
+        const int j = gtid() + bt * kGroupThreads;
+        if (j < nj) {
+            const int k = j % ns;
+            const int base = (j / ns) * ns * RADIX + k;
+#pragma unroll
+            for (int r = 0; r < RADIX; ++r) dst[pad16(base + out_slot<RADIX>(r) * ns)] = v[bt][r];
+        }
     }
     gsync();
 }
 
-// Full M-point complex FFT, M a compile-time power of two in [16, 4096]:
+// Full M-point complex FFT, M a compile-time power of two in [16, 8192]:
 // radix-16 passes, then one radix-2/4/8 pass for the remaining factor. The
 // first pass reads `src` (padded or not); later passes work in place on `buf`.
 template <int M, bool INV, bool SRC_PADDED, int NS = 1, typename V, typename TW>
 __device__ __forceinline__ void cfft(const V* src, V* buf, const TW& tw) {
     constexpr int REM = M / NS;
     if constexpr (REM >= 16) {
-        stockham_pass<16, INV, SRC_PADDED>(src, buf, M, NS, tw);
+        stockham_pass<16, INV, SRC_PADDED, M>(src, buf, NS, tw);
         cfft<M, INV, true, NS * 16>(buf, buf, tw);
     } else if constexpr (REM > 1) {
-        stockham_pass<REM, INV, SRC_PADDED>(src, buf, M, NS, tw);
+        stockham_pass<REM, INV, SRC_PADDED, M>(src, buf, NS, tw);
     }
 }
 

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kThreads) k_premf(PremfArgs a) {
     }
     double acc = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
     for (; j < cnt; ++j) acc = __dadd_rn(acc, __dmul_rn(h[j], xv[j]));
-    a.mf[((size_t)b * 32 + ch) * a.mf_len + n] = acc;
+    a.mf[((size_t)b * 32 + ch) * a.mf_stride + n] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -156,13 +156,12 @@ template <int M>
 __global__ void __launch_bounds__(kThreads) k_matched_filter(MfArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int N = 2 * M;
-    double* bufA = reinterpret_cast<double*>(smem);
-    double2* bufB = reinterpret_cast<double2*>(bufA + N);
+    double2* bufB = reinterpret_cast<double2*>(smem);
     const size_t row = (size_t)blockIdx.y * 32 + blockIdx.x;
-    const double* x = a.mf + row * a.mf_len;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) bufA[i] = i < a.mf_len ? x[i] : 0.0;
-    __syncthreads();
-    cfft<M, false, false>(reinterpret_cast<const double2*>(bufA), bufB, TwGlobal<double2>{a.tw, 2});
+    // pre-MF rows are stored zero-padded to N (stride mf_stride >= N): the
+    // first FFT pass reads them straight from global memory
+    const double* x = a.mf + row * a.mf_stride;
+    cfft<M, false, false>(reinterpret_cast<const double2*>(x), bufB, TwGlobal<double2>{a.tw, 2});
     const double scale = 2.0 / (double)N;
     const double2* R = a.ref_spec;
     real_spectral_op(bufB, M, TwGlobal<double2>{a.tw, 2}, [&](double2 X, int k) {
@@ -196,12 +195,8 @@ template <int M>
 __global__ void __launch_bounds__(kThreads) k_rfft_forward(const double* x, double2* X,
                                                            const double2* tw) {
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int N = 2 * M;
-    double* bufA = reinterpret_cast<double*>(smem);
-    double2* bufB = reinterpret_cast<double2*>(bufA + N);
-    for (int i = threadIdx.x; i < N; i += blockDim.x) bufA[i] = x[i];
-    __syncthreads();
-    cfft<M, false, false>(reinterpret_cast<const double2*>(bufA), bufB, TwGlobal<double2>{tw, 2});
+    double2* bufB = reinterpret_cast<double2*>(smem);
+    cfft<M, false, false>(reinterpret_cast<const double2*>(x), bufB, TwGlobal<double2>{tw, 2});
     for (int k = threadIdx.x; k <= M; k += blockDim.x) {
         const int k1 = k % M, k2 = (M - k) % M;
         const double2 zk = bufB[pad16(k1)], zkk = bufB[pad16(k2)];
@@ -390,7 +385,7 @@ __device__ __forceinline__ void fir_polyphase(const R* ph, const R* comp, const 
 }
 
 template <typename R, int G, int M>
-__global__ void __launch_bounds__(kThreads * G, (sizeof(R) == 8 ? SNB_ENV_MINB : SNB_ENV_MINB_F32) / G)
+__global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 ? SNB_ENV_MINB : SNB_ENV_MINB_F32) / G)
     k_envelope(EnvArgs a, FirTaps<R> taps) {
     using V = typename Cx<R>::T;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -587,7 +582,7 @@ size_t demod_smem_bytes(int octets, int words) {
 
 size_t fft_smem_bytes(int n, int real_bytes) {
     const int M = n / 2;
-    return (size_t)n * real_bytes + (size_t)(M + M / 16) * 2 * real_bytes;
+    return (size_t)(M + M / 16) * 2 * real_bytes;
 }
 
 static void set_smem(const void* fn, size_t smem) {
@@ -645,6 +640,7 @@ size_t envelope_smem_bytes(int n, int comp_taps_padded, int phase_reals, bool f3
         case 1024: { constexpr int MM = 1024; CALL; break; }             \
         case 2048: { constexpr int MM = 2048; CALL; break; }             \
         case 4096: { constexpr int MM = 4096; CALL; break; }             \
+        case 8192: { constexpr int MM = 8192; CALL; break; }             \
         default: break;                                                  \
     }
 

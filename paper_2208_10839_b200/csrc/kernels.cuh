@@ -37,19 +37,19 @@ struct DemodArgs {
 
 struct PremfArgs {
     const double* demod; // [B][32][demod_len]
-    double* mf;          // [B][32][mf_len]
+    double* mf;          // [B][32][mf_stride], samples [0, mf_len), zero tail
     const double* rev;   // premf reversed taps
-    int64_t demod_len, mf_len;
+    int64_t demod_len, mf_len, mf_stride;
     int taps, decim;
 };
 
 struct MfArgs {
-    const double* mf;       // [B][32][mf_len]
+    const double* mf;       // [B][32][mf_stride] zero-padded rows (mf_stride >= n)
     double* filt;           // [B][32][mf_len]
     float* filt32;          // optional f32 copy (F32 mode) or null
     const double2* ref_spec;// M+1 bins of rfft(reversed chirp, N)
     const double2* tw;      // e^{-2 pi i k/N}, k < N
-    int64_t mf_len, Lp;
+    int64_t mf_len, Lp, mf_stride;
     int n, ref_len, H;
     unsigned long long* amax_bits; // optional [B] max |filt| (as double bits), zeroed by the caller
 };

@@ -229,9 +229,9 @@ struct sn_workspace {
 
     void init_device() {
         const Sizes& s = plan.sz;
-        if (s.mf_fft > 8192 || s.env_fft > 8192) {
+        if (s.mf_fft > 16384 || s.env_fft > 16384) {
             config_error("pipeline: FFT size " + std::to_string(std::max(s.mf_fft, s.env_fft)) +
-                         " exceeds the shared-memory FFT limit (8192; max_range <= ~5.8 m at 4.5 MHz)");
+                         " exceeds the shared-memory FFT limit (16384; max_range <= ~11.7 m at 4.5 MHz)");
         }
         if (s.mf_fft < 32 || s.env_fft < 32) config_error("pipeline: processed window too short for the device FFT");
         DeviceGuard g(device);
@@ -248,7 +248,8 @@ struct sn_workspace {
         uint64_t& n = device_allocs;
         d_packed = dmalloc<uint8_t>(B * packed_bytes, n);
         d_demod = dmalloc<double>(B * kCh * s.demod_len, n);
-        d_mf = dmalloc<double>(B * kCh * s.mf_len, n);
+        d_mf = dmalloc<double>(B * kCh * s.mf_fft, n); // rows zero-padded to the MF FFT size
+        ck(cudaMemsetAsync(d_mf, 0, B * kCh * s.mf_fft * sizeof(double), stream), "memset");
         halo = plan.halo;
         lp = s.mf_len + 2 * static_cast<uint64_t>(halo);
         d_filt = dmalloc<double>(B * kCh * lp, n);
@@ -548,12 +549,13 @@ struct sn_workspace {
         if (profiling) cudaEventRecord(ev[0], s);
         launch_demod(da, demod_grid, demod_smem, s);
         if (profiling) cudaEventRecord(ev[1], s);
-        PremfArgs pa{d_demod, d_mf, d_premf, (int64_t)z.demod_len, (int64_t)z.mf_len,
+        PremfArgs pa{d_demod, d_mf, d_premf, (int64_t)z.demod_len, (int64_t)z.mf_len, (int64_t)z.mf_fft,
                      (int)plan.premf_rev.size(), plan.cfg.pre_mf_decimation};
         launch_premf(pa, (int)count, s);
         if (profiling) cudaEventRecord(ev[2], s);
         MfArgs ma{d_mf, d_filt, f32 && !tc ? d_filt32 : nullptr, d_ref_spec, d_tw_mf,
-                  (int64_t)z.mf_len, (int64_t)lp, (int)z.mf_fft, (int)z.ref_len, halo, tc ? d_amax : nullptr};
+                  (int64_t)z.mf_len, (int64_t)lp, (int64_t)z.mf_fft, (int)z.mf_fft, (int)z.ref_len, halo,
+                  tc ? d_amax : nullptr};
         if (tc) ck(cudaMemsetAsync(d_amax, 0, count * sizeof(unsigned long long), s), "memset");
         launch_matched_filter(ma, (int)count, mf_smem, s);
         if (profiling) cudaEventRecord(ev[3], s);
@@ -1053,15 +1055,16 @@ sn_status sn_workspace_stage(sn_workspace* ws, int32_t stage, uint64_t item, dou
         uint64_t n = 0;
         switch (stage) {
             case SN_STAGE_DEMOD: src = ws->d_demod + item * kCh * z.demod_len; n = kCh * z.demod_len; break;
-            case SN_STAGE_PREMF: src = ws->d_mf + item * kCh * z.mf_len; n = kCh * z.mf_len; break;
+            case SN_STAGE_PREMF: src = ws->d_mf + item * kCh * z.mf_fft; n = kCh * z.mf_len; break;
             case SN_STAGE_FILT: src = ws->d_filt + item * kCh * ws->lp + ws->halo; n = kCh * z.mf_len; break;
             default: argument_error("unknown stage");
         }
         if (capacity < n) argument_error("buffer too small");
         DeviceGuard g(ws->device);
         ck(cudaStreamSynchronize(ws->stream), "sync");
-        if (stage == SN_STAGE_FILT) {
-            ck(cudaMemcpy2D(out, z.mf_len * sizeof(double), src, ws->lp * sizeof(double),
+        if (stage == SN_STAGE_FILT || stage == SN_STAGE_PREMF) {
+            const uint64_t pitch = stage == SN_STAGE_FILT ? ws->lp : z.mf_fft;
+            ck(cudaMemcpy2D(out, z.mf_len * sizeof(double), src, pitch * sizeof(double),
                             z.mf_len * sizeof(double), kCh, cudaMemcpyDeviceToHost), "stage copy");
         } else {
             ck(cudaMemcpy(out, src, n * sizeof(double), cudaMemcpyDeviceToHost), "stage copy");

@@ -42,6 +42,8 @@ def cfg_for(sn, name, precision=0):
         "box1850": lambda: sn.default_pipeline_config(sn.GridKind.box1850),
         "hemi3000": lambda: sn.default_pipeline_config(sn.GridKind.hemisphere3000),
         "small_box": lambda: sn.default_pipeline_config(sn.GridKind.box1850).copy(max_range=1.5),
+        "h90_10m": lambda: base.copy(max_range=10.0),
+        "box_8m": lambda: sn.default_pipeline_config(sn.GridKind.box1850).copy(max_range=8.0),
     }
     return cfgs[name]().copy(precision=precision)
 
@@ -94,7 +96,8 @@ def test_golden_h90(gpu, po):
     assert same >= 0.999, same
 
 
-@pytest.mark.parametrize("name", ["small", "h90", "az181", "box1850", "hemi3000", "small_box"])
+@pytest.mark.parametrize("name", ["small", "h90", "az181", "box1850", "hemi3000", "small_box", "h90_10m",
+                                  "box_8m"])
 def test_parity_vs_reference_f64(gpu, po, ref, name):
     sn = gpu
     cfg = cfg_for(sn, name)
