@@ -540,7 +540,7 @@ struct sn_workspace {
     }
 
     // Enqueue the whole pipeline for `count` measurements (count <= max_batch).
-    void enqueue(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s) {
+    void enqueue(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s, bool with_envelope = true) {
         const Sizes& z = plan.sz;
         DemodArgs da = demod;
         da.packed = d_in;
@@ -597,8 +597,19 @@ struct sn_workspace {
         launch_beamform_tiles(ba, f32, s);
         }
         if (profiling) cudaEventRecord(ev[4], s);
+        if (with_envelope) enqueue_envelope(0, count, d_out, s);
+        if (profiling) cudaEventRecord(ev[5], s);
+        ck(cudaGetLastError(), "kernel launch");
+        last_launches = tc ? 6 : 5;
+    }
+
+    // Envelope stage for captures [b0, b0 + count) of the batch whose beams
+    // are in d_beams; energies to d_out (capture b0 first).
+    void enqueue_envelope(uint64_t b0, uint64_t count, float* d_out, cudaStream_t s) {
+        const Sizes& z = plan.sz;
+        const size_t rb = f32 ? sizeof(float) : sizeof(double);
         EnvArgs ea{};
-        ea.beams = d_beams;
+        ea.beams = static_cast<const uint8_t*>(d_beams) + b0 * z.n_dirs * z.env_fft * rb;
         ea.energy = d_out;
         ea.order = d_order;
         ea.comp = f32 ? (const void*)d_comp32 : (const void*)d_comp;
@@ -615,9 +626,6 @@ struct sn_workspace {
         ea.phase_len = phase_len;
         ea.fir_fast = fir_fast;
         launch_envelope(ea, taps32, taps64, f32, dir_grid, s);
-        if (profiling) cudaEventRecord(ev[5], s);
-        ck(cudaGetLastError(), "kernel launch");
-        last_launches = tc ? 6 : 5;
     }
 
     void validate(const sn_raw_measurement& m) const { // pipeline.cpp:524-540
@@ -664,22 +672,27 @@ struct sn_workspace {
         uint64_t done = 0;
         while (done < count) {
             const uint64_t c = std::min(max_batch, count - done);
+            // all captures up (copy stream), the front end + beamformer for the
+            // whole block, then the envelope in chunks whose energyscapes are
+            // downloaded (D2H stream) while the next chunk computes: only the
+            // upload and the last chunk's download are exposed
+            for (uint64_t i = 0; i < c; ++i) {
+                const uint8_t* src = ms[done + i].packed;
+                if (!is_pinned(src)) {
+                    std::memcpy(h_in + i * packed_bytes, src, packed_bytes);
+                    src = h_in + i * packed_bytes;
+                }
+                ck(cudaMemcpyAsync(d_packed + i * packed_bytes, src, packed_bytes, cudaMemcpyHostToDevice, s_h2d),
+                   "H2D");
+            }
+            ck(cudaEventRecord(ev_in[0], s_h2d), "event");
+            ck(cudaStreamWaitEvent(stream, ev_in[0], 0), "wait");
+            enqueue(d_packed, c, d_energy, stream, /*with_envelope=*/false);
             const uint64_t nch = std::min<uint64_t>(c, kMaxChunks);
             uint64_t off = 0;
             for (uint64_t j = 0; j < nch; ++j) {
                 const uint64_t k = c / nch + (j < c % nch ? 1 : 0); // captures in chunk j
-                for (uint64_t i = off; i < off + k; ++i) {
-                    const uint8_t* src = ms[done + i].packed;
-                    if (!is_pinned(src)) {
-                        std::memcpy(h_in + i * packed_bytes, src, packed_bytes);
-                        src = h_in + i * packed_bytes;
-                    }
-                    ck(cudaMemcpyAsync(d_packed + i * packed_bytes, src, packed_bytes,
-                                       cudaMemcpyHostToDevice, s_h2d), "H2D");
-                }
-                ck(cudaEventRecord(ev_in[j], s_h2d), "event");
-                ck(cudaStreamWaitEvent(stream, ev_in[j], 0), "wait");
-                enqueue(d_packed + off * packed_bytes, k, d_energy + off * energy_per, stream);
+                enqueue_envelope(off, k, d_energy + off * energy_per, stream);
                 ck(cudaEventRecord(ev_done[j], stream), "event");
                 ck(cudaStreamWaitEvent(s_d2h, ev_done[j], 0), "wait");
                 float* dst = (out_pinned ? out + done * energy_per : h_out) + off * energy_per;
@@ -687,6 +700,8 @@ struct sn_workspace {
                                    cudaMemcpyDeviceToHost, s_d2h), "D2H");
                 off += k;
             }
+            ck(cudaGetLastError(), "kernel launch");
+            last_launches = (tc ? 5 : 4) + nch;
             ck(cudaStreamSynchronize(s_d2h), "process sync");
             if (!out_pinned) std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
             done += c;
