@@ -766,24 +766,36 @@ struct sn_workspace {
                                 nin, false, d_crc_ok, stream);
             ck(cudaMemcpy2DAsync(d_packed, packed_bytes, d_frames_in + 74, in_frame_stride, packed_bytes, c,
                                  cudaMemcpyDeviceToDevice, stream), "D2D packed");
-            enqueue(d_packed, c, d_energy, stream);
-            ImageFrameArgs ia{d_energy, d_img_tpl, d_ids, d_frames_out, d_crc_acc + max_batch, energy_per,
-                              img_tpl_len, img_frame_len, img_frame_stride};
-            launch_encode_image_frames(ia, c, ct, stream);
-            const uint64_t nout = img_frame_len - 4;
-            launch_crc_finalize(d_crc_acc + max_batch, crc_init_term(h_crc_shift.data(), nout), c, d_frames_out,
-                                img_frame_stride, nout, true, nullptr, stream);
-            ck(cudaGetLastError(), "frame kernels");
-            // D2H straight into the caller's slots when they are page-locked
-            // (consecutive batch entries are consecutive slots in the common case)
+            enqueue(d_packed, c, d_energy, stream, /*with_envelope=*/false);
+            // envelope + frame encode in chunks; each chunk's frames download
+            // (D2H stream) while the next chunk computes. D2H straight into the
+            // caller's slots when they are page-locked and consecutive.
             const bool direct = out_pinned && batch.back() - batch.front() == c - 1;
-            if (direct) {
-                ck(cudaMemcpy2DAsync(out + batch.front() * slot, slot, d_frames_out, img_frame_stride, img_frame_len, c,
-                                     cudaMemcpyDeviceToHost, stream), "D2H frames");
-            } else {
-                ck(cudaMemcpy2DAsync(h_frames_out, img_frame_len, d_frames_out, img_frame_stride, img_frame_len, c,
-                                     cudaMemcpyDeviceToHost, stream), "D2H frames");
+            const uint64_t nout = img_frame_len - 4;
+            const uint32_t kout = crc_init_term(h_crc_shift.data(), nout);
+            const uint64_t nch = std::min<uint64_t>(c, kMaxChunks);
+            uint64_t off = 0;
+            for (uint64_t j = 0; j < nch; ++j) {
+                const uint64_t k = c / nch + (j < c % nch ? 1 : 0);
+                enqueue_envelope(off, k, d_energy + off * energy_per, stream);
+                ImageFrameArgs ia{d_energy + off * energy_per, d_img_tpl, d_ids + off,
+                                  d_frames_out + off * img_frame_stride, d_crc_acc + max_batch + off, energy_per,
+                                  img_tpl_len, img_frame_len, img_frame_stride};
+                launch_encode_image_frames(ia, k, ct, stream);
+                launch_crc_finalize(d_crc_acc + max_batch + off, kout, k, d_frames_out + off * img_frame_stride,
+                                    img_frame_stride, nout, true, nullptr, stream);
+                ck(cudaEventRecord(ev_done[j], stream), "event");
+                ck(cudaStreamWaitEvent(s_d2h, ev_done[j], 0), "wait");
+                uint8_t* dst = direct ? out + (batch.front() + off) * slot : h_frames_out + off * img_frame_len;
+                const uint64_t dpitch = direct ? slot : img_frame_len;
+                for (uint64_t i = 0; i < k; ++i) {
+                    ck(cudaMemcpyAsync(dst + i * dpitch, d_frames_out + (off + i) * img_frame_stride, img_frame_len,
+                                       cudaMemcpyDeviceToHost, s_d2h), "D2H frame");
+                }
+                off += k;
             }
+            ck(cudaGetLastError(), "frame kernels");
+            ck(cudaStreamSynchronize(s_d2h), "frames sync");
             ck(cudaMemcpyAsync(h_crc_ok, d_crc_ok, c * sizeof(int32_t), cudaMemcpyDeviceToHost, stream), "D2H ok");
             ck(cudaStreamSynchronize(stream), "frames sync");
             for (uint64_t i = 0; i < c; ++i) {
