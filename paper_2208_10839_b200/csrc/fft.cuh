@@ -176,6 +176,10 @@ template <typename V> struct TwShared {
 // with radix 16, 2 for M = 8192).
 template <int RADIX, bool INV, bool SRC_PADDED, int M, typename V, typename TW>
 __device__ __forceinline__ void stockham_pass(const V* src, V* dst, int ns, const TW& tw) {
+    // SRC_PADDED: in place in the shared buffer, so every thread's loads must
+    // finish before any store (barrier below). Otherwise src is a different
+    // (global) array and dst is free (callers end their previous use of the
+    // buffer with a barrier): no pre-store barrier.
     constexpr int nj = M / RADIX;
     constexpr int BPT = (nj + kGroupThreads - 1) / kGroupThreads;
     V v[BPT][RADIX];
@@ -218,7 +222,7 @@ __device__ __forceinline__ void stockham_pass(const V* src, V* dst, int ns, cons
             dft_r<RADIX, INV>(v[bt]);
         }
     }
-    gsync();
+    if constexpr (SRC_PADDED) gsync();
 #pragma unroll
     for (int bt = 0; bt < BPT; ++bt) {
         const int j = gtid() + bt * kGroupThreads;

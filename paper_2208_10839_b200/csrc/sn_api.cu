@@ -117,7 +117,21 @@ struct sn_workspace {
     // host path: copies run on their own streams so that chunk j+1's H2D and
     // chunk j-1's D2H overlap chunk j's kernels
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-    static constexpr int kMaxChunks = 8;
+    static constexpr int kMaxChunks = 16;
+    // envelope chunk sizes of a block of c captures: ~2 per chunk, the last
+    // chunk a single capture (its download is the exposed one)
+    static std::vector<uint64_t> env_chunks(uint64_t c) {
+        std::vector<uint64_t> v;
+        if (c <= 2) {
+            v.assign(c, 1);
+            return v;
+        }
+        uint64_t rest = c - 1;
+        const uint64_t n = std::min<uint64_t>((rest + 1) / 2, kMaxChunks - 1);
+        for (uint64_t j = 0; j < n; ++j) v.push_back(rest / n + (j < rest % n ? 1 : 0));
+        v.push_back(1);
+        return v;
+    }
     cudaEvent_t ev_in[kMaxChunks] = {}, ev_done[kMaxChunks] = {};
     bool f32 = false;
     // device buffers
@@ -688,10 +702,11 @@ struct sn_workspace {
             ck(cudaEventRecord(ev_in[0], s_h2d), "event");
             ck(cudaStreamWaitEvent(stream, ev_in[0], 0), "wait");
             enqueue(d_packed, c, d_energy, stream, /*with_envelope=*/false);
-            const uint64_t nch = std::min<uint64_t>(c, kMaxChunks);
+            const std::vector<uint64_t> chunks = env_chunks(c);
+            const uint64_t nch = chunks.size();
             uint64_t off = 0;
             for (uint64_t j = 0; j < nch; ++j) {
-                const uint64_t k = c / nch + (j < c % nch ? 1 : 0); // captures in chunk j
+                const uint64_t k = chunks[j]; // captures in chunk j
                 enqueue_envelope(off, k, d_energy + off * energy_per, stream);
                 ck(cudaEventRecord(ev_done[j], stream), "event");
                 ck(cudaStreamWaitEvent(s_d2h, ev_done[j], 0), "wait");
@@ -773,10 +788,11 @@ struct sn_workspace {
             const bool direct = out_pinned && batch.back() - batch.front() == c - 1;
             const uint64_t nout = img_frame_len - 4;
             const uint32_t kout = crc_init_term(h_crc_shift.data(), nout);
-            const uint64_t nch = std::min<uint64_t>(c, kMaxChunks);
+            const std::vector<uint64_t> chunks = env_chunks(c);
+            const uint64_t nch = chunks.size();
             uint64_t off = 0;
             for (uint64_t j = 0; j < nch; ++j) {
-                const uint64_t k = c / nch + (j < c % nch ? 1 : 0);
+                const uint64_t k = chunks[j];
                 enqueue_envelope(off, k, d_energy + off * energy_per, stream);
                 ImageFrameArgs ia{d_energy + off * energy_per, d_img_tpl, d_ids + off,
                                   d_frames_out + off * img_frame_stride, d_crc_acc + max_batch + off, energy_per,
