@@ -594,7 +594,92 @@ void launch_demod(const DemodArgs& a, int grid_x, size_t smem, cudaStream_t s) {
     k_demod<<<dim3(grid_x, a.period), kThreads, smem, s>>>(a);
 }
 
+// ---------------------------------------------------------------------------
+// k_premf_rw: the same filter for the reference's default (65 taps, /2), with
+// a register window: a thread computes kPremfR consecutive outputs, whose
+// 65-sample windows overlap in all but 2 samples, so 2 R + 63 loads serve
+// 65 R products; taps are kernel-parameter (constant-bank) operands. Each
+// output keeps the reference's exact order (lane j mod 4 over j < 64, then
+// (a0 + a1) + (a2 + a3), then j = 64; rounded products, no FMA). Blocks
+// whose windows are clipped by the row ends take the generic loop.
+// ---------------------------------------------------------------------------
+constexpr int kPremfTaps = 65, kPremfR = 8, kPremfThreads = 128;
+struct PremfTaps { double h[kPremfTaps]; };
+
+// the CTA's input span staged in shared memory with one pad double per 16
+// (thread t reads from 16 t + j: stride 17, bank-conflict free)
+__device__ __forceinline__ int premf_pad(int i) { return i + (i >> 4); }
+
+__global__ void __launch_bounds__(kPremfThreads) k_premf_rw(PremfArgs a, const __grid_constant__ PremfTaps t) {
+    constexpr int kSpan = 2 * kPremfThreads * kPremfR + kPremfTaps; // inputs of the CTA's outputs
+    __shared__ double xs[kSpan + kSpan / 16 + 1];
+    const int ch = blockIdx.y, b = blockIdx.z;
+    const int64_t nb = (int64_t)blockIdx.x * kPremfThreads * kPremfR;
+    const int64_t n0 = nb + (int64_t)threadIdx.x * kPremfR;
+    const double* x = a.demod + ((size_t)b * 32 + ch) * a.demod_len;
+    double* out = a.mf + ((size_t)b * 32 + ch) * a.mf_stride;
+    constexpr int start = -(kPremfTaps - 1) / 2;
+    const int64_t sb = start + 2 * nb;
+    for (int i = threadIdx.x; i < kSpan; i += kPremfThreads) {
+        const int64_t g = sb + i;
+        xs[premf_pad(i)] = (g >= 0 && g < a.demod_len) ? x[g] : 0.0;
+    }
+    __syncthreads();
+    if (n0 >= a.mf_len) return;
+    const int64_t s0 = start + 2 * n0;
+    if (s0 >= 0 && s0 + 2 * (kPremfR - 1) + kPremfTaps <= a.demod_len && n0 + kPremfR <= a.mf_len) {
+        const int l0 = (int)(s0 - sb); // = 2 kPremfR threadIdx.x
+        double acc[kPremfR][4];
+#pragma unroll
+        for (int r = 0; r < kPremfR; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.0;
+        double w[2 * kPremfR + kPremfTaps];
+#pragma unroll
+        for (int i = 0; i < 2 * kPremfR - 2; ++i) w[i] = xs[premf_pad(l0 + i)];
+#pragma unroll
+        for (int j = 0; j < kPremfTaps - 1; ++j) {
+            w[2 * kPremfR - 2 + j] = xs[premf_pad(l0 + 2 * kPremfR - 2 + j)];
+#pragma unroll
+            for (int r = 0; r < kPremfR; ++r) acc[r][j & 3] = __dadd_rn(acc[r][j & 3], __dmul_rn(t.h[j], w[2 * r + j]));
+        }
+        w[2 * kPremfR - 2 + kPremfTaps - 1] = xs[premf_pad(l0 + 2 * kPremfR - 2 + kPremfTaps - 1)];
+#pragma unroll
+        for (int r = 0; r < kPremfR; ++r) {
+            double v = __dadd_rn(__dadd_rn(acc[r][0], acc[r][1]), __dadd_rn(acc[r][2], acc[r][3]));
+            v = __dadd_rn(v, __dmul_rn(t.h[kPremfTaps - 1], w[2 * r + kPremfTaps - 1]));
+            out[n0 + r] = v;
+        }
+        return;
+    }
+    // clipped windows (row ends): generic per-output loop, same order
+    for (int r = 0; r < kPremfR; ++r) {
+        const int64_t n = n0 + r;
+        if (n >= a.mf_len) break;
+        const int64_t s = start + 2 * n;
+        const int64_t lo = s > 0 ? s : 0, hi = (s + kPremfTaps) < a.demod_len ? (s + kPremfTaps) : a.demod_len;
+        const int cnt = (int)(hi - lo);
+        const int h0 = (int)(lo - s);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int j = 0;
+        for (; j + 4 <= cnt; j += 4) {
+            a0 = __dadd_rn(a0, __dmul_rn(t.h[h0 + j], x[lo + j]));
+            a1 = __dadd_rn(a1, __dmul_rn(t.h[h0 + j + 1], x[lo + j + 1]));
+            a2 = __dadd_rn(a2, __dmul_rn(t.h[h0 + j + 2], x[lo + j + 2]));
+            a3 = __dadd_rn(a3, __dmul_rn(t.h[h0 + j + 3], x[lo + j + 3]));
+        }
+        double acc = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+        for (; j < cnt; ++j) acc = __dadd_rn(acc, __dmul_rn(t.h[h0 + j], x[lo + j]));
+        out[n] = acc;
+    }
+}
+
 void launch_premf(const PremfArgs& a, int batch, cudaStream_t s) {
+    if (a.taps == kPremfTaps && a.decim == 2 && a.rev_host) {
+        PremfTaps t;
+        for (int i = 0; i < kPremfTaps; ++i) t.h[i] = a.rev_host[i];
+        const int64_t per = (int64_t)kPremfThreads * kPremfR;
+        k_premf_rw<<<dim3((unsigned)((a.mf_len + per - 1) / per), 32, batch), kPremfThreads, 0, s>>>(a, t);
+        return;
+    }
     const size_t smem = (size_t)(a.taps + (kThreads - 1) * a.decim + a.taps) * sizeof(double);
     set_smem((const void*)k_premf, smem);
     const int gx = (int)((a.mf_len + kThreads - 1) / kThreads);

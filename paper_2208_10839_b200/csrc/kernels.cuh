@@ -41,6 +41,7 @@ struct PremfArgs {
     const double* rev;   // premf reversed taps
     int64_t demod_len, mf_len, mf_stride;
     int taps, decim;
+    const double* rev_host; // the same taps on the host (register-window kernel params) or null
 };
 
 struct MfArgs {

@@ -564,7 +564,7 @@ struct sn_workspace {
         launch_demod(da, demod_grid, demod_smem, s);
         if (profiling) cudaEventRecord(ev[1], s);
         PremfArgs pa{d_demod, d_mf, d_premf, (int64_t)z.demod_len, (int64_t)z.mf_len, (int64_t)z.mf_fft,
-                     (int)plan.premf_rev.size(), plan.cfg.pre_mf_decimation};
+                     (int)plan.premf_rev.size(), plan.cfg.pre_mf_decimation, plan.premf_rev.data()};
         launch_premf(pa, (int)count, s);
         if (profiling) cudaEventRecord(ev[2], s);
         MfArgs ma{d_mf, d_filt, f32 && !tc ? d_filt32 : nullptr, d_ref_spec, d_tw_mf,
