@@ -409,8 +409,17 @@ Plan make_plan(const sn_pipeline_config& cin) {
         std::iota(idx.begin(), idx.end(), 0);
         std::vector<int32_t> leaves;
         leaves.reserve(s.n_dirs);
-        auto split = [&](auto&& self, int32_t* b, int32_t* e) -> void {
+        // two levels: subtrees of <= kTcLeafDirs directions (filled to
+        // kTcLeafDirs where possible: the tensor-core beamformer's clusters,
+        // compact in direction space so their per-channel shift spans stay
+        // small), each split further into kClusterDirs leaves
+        std::vector<int32_t> tc_leaves;
+        auto split = [&](auto&& self, int32_t* b, int32_t* e, bool in_tc) -> void {
             const int64_t n = e - b;
+            if (!in_tc && n <= kTcLeafDirs) {
+                tc_leaves.push_back((int32_t)leaves.size());
+                in_tc = true;
+            }
             if (n <= kClusterDirs) {
                 leaves.insert(leaves.end(), b, e);
                 return;
@@ -424,11 +433,15 @@ Plan make_plan(const sn_pipeline_config& cin) {
             }
             const std::vector<double>& key = (yhi - ylo >= zhi - zlo) ? uy : uz;
             std::stable_sort(b, e, [&](int32_t x, int32_t y) { return key[x] < key[y]; });
-            const int64_t nl = kClusterDirs * ((n + 2 * kClusterDirs - 1) / (2 * kClusterDirs));
-            self(self, b, b + nl);
-            self(self, b + nl, e);
+            const int64_t unit = in_tc ? kClusterDirs : kTcLeafDirs;
+            int64_t nl = unit * ((n + 2 * unit - 1) / (2 * unit));
+            if (nl >= n) nl = n / 2;
+            self(self, b, b + nl, in_tc);
+            self(self, b + nl, e, in_tc);
         };
-        split(split, idx.data(), idx.data() + idx.size());
+        split(split, idx.data(), idx.data() + idx.size(), false);
+        tc_leaves.push_back((int32_t)s.n_dirs);
+        p.tc_leaves = std::move(tc_leaves);
         std::vector<std::pair<uint64_t, int32_t>> keyed(s.n_dirs);
         for (uint64_t k = 0; k < s.n_dirs; ++k) keyed[k] = {k, leaves[k]};
         p.order.resize(s.n_dirs);

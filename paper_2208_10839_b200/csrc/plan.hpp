@@ -52,10 +52,12 @@ struct Plan {
     // direction is independent, pipeline.cpp:225-226):
     std::vector<int32_t> order;       // slot -> direction, Morton order of (u_y, u_z)
     std::vector<int32_t> shifts;      // slot-major [n_dirs][32]: delay - advance
+    std::vector<int32_t> tc_leaves;   // first slot of every <= kTcLeafDirs k-d subtree (+ n_dirs)
     int32_t halo = 0;                 // max |shift| over all directions/channels
 };
 
-constexpr int kClusterDirs = 8; // k-d leaf size of the direction schedule
+constexpr int kClusterDirs = 8;  // k-d leaf size of the direction schedule
+constexpr int kTcLeafDirs = 128; // upper k-d level: tensor-core beamformer clusters
 
 // Validates (pipeline.cpp:60-92; geometry.cpp:27-57 invariants; Direction
 // ranges geometry.cpp:146-155) and derives every table. Throws Error.

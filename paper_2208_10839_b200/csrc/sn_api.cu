@@ -470,39 +470,44 @@ struct sn_workspace {
         tc_start.clear();
         tc_size.clear();
         tc_resid.clear();
-        uint64_t s0 = 0;
-        while (s0 < nd) {
-            int lo[kCh], hi[kCh];
-            for (int i = 0; i < kCh; ++i) { lo[i] = 1 << 30; hi[i] = -(1 << 30); }
-            uint64_t s1 = s0;
-            int R = 1;
-            while (s1 < nd && s1 - s0 < (uint64_t)kTcM) {
-                int Rn = 1;
-                for (int i = 0; i < kCh; ++i) {
-                    const int v = plan.shifts[s1 * kCh + i];
-                    Rn = std::max(Rn, std::max(hi[i], v) - std::min(lo[i], v) + 1);
+        // clusters: the planner's <= 128-direction k-d subtrees, each cut
+        // greedily further only if its shift span exceeds kTcRMax
+        for (size_t leaf = 0; leaf + 1 < plan.tc_leaves.size(); ++leaf) {
+            uint64_t s0 = (uint64_t)plan.tc_leaves[leaf];
+            const uint64_t s_end = (uint64_t)plan.tc_leaves[leaf + 1];
+            while (s0 < s_end) {
+                int lo[kCh], hi[kCh];
+                for (int i = 0; i < kCh; ++i) { lo[i] = 1 << 30; hi[i] = -(1 << 30); }
+                uint64_t s1 = s0;
+                int R = 1;
+                while (s1 < s_end && s1 - s0 < (uint64_t)kTcM) {
+                    int Rn = 1;
+                    for (int i = 0; i < kCh; ++i) {
+                        const int v = plan.shifts[s1 * kCh + i];
+                        Rn = std::max(Rn, std::max(hi[i], v) - std::min(lo[i], v) + 1);
+                    }
+                    if (Rn > kTcRMax) break;
+                    for (int i = 0; i < kCh; ++i) {
+                        const int v = plan.shifts[s1 * kCh + i];
+                        lo[i] = std::min(lo[i], v);
+                        hi[i] = std::max(hi[i], v);
+                    }
+                    R = Rn;
+                    ++s1;
                 }
-                if (Rn > kTcRMax) break;
-                for (int i = 0; i < kCh; ++i) {
-                    const int v = plan.shifts[s1 * kCh + i];
-                    lo[i] = std::min(lo[i], v);
-                    hi[i] = std::max(hi[i], v);
+                const size_t c = tc_R.size();
+                tc_R.push_back(R);
+                tc_start.push_back((int32_t)s0);
+                tc_size.push_back((int32_t)(s1 - s0));
+                tc_base.resize((c + 1) * kCh);
+                tc_resid.resize((c + 1) * kTcM * kCh, 0xFF);
+                for (int i = 0; i < kCh; ++i) tc_base[c * kCh + i] = lo[i];
+                for (uint64_t sl = s0; sl < s1; ++sl) {
+                    for (int i = 0; i < kCh; ++i)
+                        tc_resid[(c * kTcM + (sl - s0)) * kCh + i] = (uint8_t)(plan.shifts[sl * kCh + i] - lo[i]);
                 }
-                R = Rn;
-                ++s1;
+                s0 = s1;
             }
-            const size_t c = tc_R.size();
-            tc_R.push_back(R);
-            tc_start.push_back((int32_t)s0);
-            tc_size.push_back((int32_t)(s1 - s0));
-            tc_base.resize((c + 1) * kCh);
-            tc_resid.resize((c + 1) * kTcM * kCh, 0xFF);
-            for (int i = 0; i < kCh; ++i) tc_base[c * kCh + i] = lo[i];
-            for (uint64_t sl = s0; sl < s1; ++sl) {
-                for (int i = 0; i < kCh; ++i)
-                    tc_resid[(c * kTcM + (sl - s0)) * kCh + i] = (uint8_t)(plan.shifts[sl * kCh + i] - lo[i]);
-            }
-            s0 = s1;
         }
         tc_clusters = (int)tc_R.size();
         tc_rmax = *std::max_element(tc_R.begin(), tc_R.end());
