@@ -163,6 +163,15 @@ sn_status sn_config_dims(const sn_pipeline_config* cfg, sn_dims* dims);
 sn_status sn_synthesize_packed(const sn_pipeline_config* cfg, const sn_scene* scene,
                                uint8_t* packed_out, uint64_t capacity);
 
+/* Synthetic captures on the GPU (load generation): `count` scenes (each with
+ * its own seed, <= 8 reflectors) -> count x (32 * frames / 8) packed bytes in
+ * DEVICE memory on `device`, identical to sn_synthesize_packed (synth.cpp:
+ * 116-134) up to last-place differences of the device log() (a sigma-delta
+ * decision changes only where |integrator + x| < ~1e-16). One capture per
+ * GPU thread (the noise stream is sequential); a batch runs in parallel. */
+sn_status sn_synthesize_device(const sn_pipeline_config* cfg, const sn_scene* scenes, uint64_t count, int device,
+                               uint8_t* d_packed, void* stream);
+
 /* ---- workspace (Workspace, pipeline.hpp:98-130) ------------------------ */
 /* device >= 0: allocate every device buffer on that CUDA device (no
  * allocation ever happens later). device < 0: host tables only (setup

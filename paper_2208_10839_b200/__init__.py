@@ -33,7 +33,7 @@ __all__ = [
     "GridKind", "Precision", "PipelineConfig", "RawMeasurement", "AcousticImage", "Reflector",
     "Scene", "Workspace", "default_pipeline_config", "direction_grid", "default_array",
     "synthesize_measurement", "SonarError", "ConfigError", "ArgumentError", "DecodeError",
-    "IoError", "CudaError", "lib", "crc32", "measurement_frame", "CentralPool",
+    "IoError", "CudaError", "lib", "crc32", "measurement_frame", "CentralPool", "synthesize_device",
 ]
 
 
@@ -192,6 +192,7 @@ def lib() -> C.CDLL:
                                     C.POINTER(C.c_uint32), C.POINTER(u64)]
     L.sn_pool_frame_bytes.restype = u64
     L.sn_pool_frame_bytes.argtypes = [vp]
+    L.sn_synthesize_device.argtypes = [C.POINTER(_Config), C.POINTER(_Scene), u64, C.c_int, vp, vp]
     L.sn_crc32.restype = C.c_uint32
     L.sn_crc32.argtypes = [vp, u64]
     L.sn_measurement_frame.argtypes = [C.POINTER(_Measurement), vp, u64, C.POINTER(u64)]
@@ -422,6 +423,24 @@ def synthesize_measurement(cfg: PipelineConfig, scene: Scene, serial: int = 1,
     out = np.zeros(32 * frames // 8, np.uint8)
     _check(lib().sn_synthesize_packed(C.byref(st), C.byref(sc), out.ctypes.data, out.size))
     return RawMeasurement(serial, timestamp_us, seq, 32, frames, cfg.pdm_rate, out)
+
+
+def synthesize_device(cfg: PipelineConfig, scenes: Sequence[Scene], d_packed_ptr: int, device: int = 0,
+                      stream: int = 0) -> None:
+    """GPU load generator (sn_synthesize_device): len(scenes) packed captures
+    (32 * frames / 8 bytes each, synth.cpp:116-134) written to device memory at
+    d_packed_ptr, one capture per GPU thread."""
+    st, _k = cfg._struct()
+    n = len(scenes)
+    keep = []
+    arr = (_Scene * max(1, n))()
+    for i, sc in enumerate(scenes):
+        refl = (_Reflector * max(1, len(sc.reflectors)))()
+        for k, r in enumerate(sc.reflectors):
+            refl[k] = _Reflector(r.range, r.azimuth, r.elevation, r.reflectivity)
+        keep.append(refl)
+        arr[i] = _Scene(refl, len(sc.reflectors), sc.noise_rms, sc.seed)
+    _check(lib().sn_synthesize_device(C.byref(st), arr, n, device, d_packed_ptr, stream))
 
 
 @dataclass

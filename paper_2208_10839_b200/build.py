@@ -31,7 +31,7 @@ HOST_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wext
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                      "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v"]
 
-CU_SOURCES = ["kernels.cu", "beamform_tc.cu", "frames.cu", "sn_api.cu"]
+CU_SOURCES = ["kernels.cu", "beamform_tc.cu", "frames.cu", "synth.cu", "sn_api.cu"]
 CPP_SOURCES = ["plan.cpp", "pool.cpp"]
 HEADERS = ["fft.cuh", "kernels.cuh", "plan.hpp"]
 

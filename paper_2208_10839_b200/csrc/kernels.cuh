@@ -132,6 +132,25 @@ void launch_encode_image_frames(const ImageFrameArgs& a, uint64_t count, const C
 void launch_crc_finalize(uint32_t* acc, uint32_t k_n, uint64_t count, uint8_t* out, uint64_t stride, uint64_t n,
                          bool store, int32_t* ok, cudaStream_t s);
 uint32_t crc32_host(const uint8_t* p, uint64_t n);
+
+// ---- synthetic captures on the GPU (synth.cu) -------------------------------
+constexpr int kSynthMaxReflectors = 8;
+struct SynthScene {
+    uint64_t seed;
+    double noise_rms;
+    int n_refl;
+    double amp[kSynthMaxReflectors];
+    int64_t onset[kSynthMaxReflectors][32];
+};
+struct SynthArgs {
+    const double* pulse;        // PDM-rate pulse (ref_len)
+    const SynthScene* scenes;   // [count]
+    uint32_t* words;            // [count][32][nwords] scratch
+    uint8_t* packed;            // [count][packed_bytes]
+    int64_t frames, ref_len, nwords, packed_bytes;
+    int count;
+};
+void launch_synth(const SynthArgs& a, cudaStream_t s);
 void crc_tables_host(uint32_t* slice, uint32_t* shift);
 uint32_t crc_init_term(const uint32_t* shift, uint64_t n);
 

@@ -471,15 +471,16 @@ Plan make_plan(const sn_pipeline_config& cin) {
     return p;
 }
 
-void synthesize_packed(const sn_pipeline_config& c, const sn_scene& scene, uint8_t* out) {
-    // synth.cpp:116-134 = synthesize_scene (:11-61) -> sigma_delta (:63-94) -> pack (:96-114)
+SceneEchoes scene_echoes(const sn_pipeline_config& c, const sn_scene& scene) {
+    // synthesize_scene (synth.cpp:11-61): per reflector the amplitude and the
+    // per-channel onset of the pulse at the PDM rate
     const Sizes s = derive_sizes(c);
     check_geometry(c);
     if (scene.noise_rms < 0.0) argument_error("synthesize_scene: noise_rms < 0");
-    const uint64_t n = s.frames;
-    const std::vector<double> pulse = chirp(c, c.pdm_rate);
-    const auto ref_len = static_cast<int64_t>(pulse.size());
-    std::vector<double> x(static_cast<size_t>(kCh) * n, 0.0);
+    SceneEchoes e;
+    e.frames = s.frames;
+    e.pulse = chirp(c, c.pdm_rate);
+    const auto ref_len = static_cast<int64_t>(e.pulse.size());
     for (uint64_t k = 0; k < scene.n_reflectors; ++k) {
         const sn_reflector& r = scene.reflectors[k];
         if (!(r.range > 0.0)) argument_error("reflector " + std::to_string(k) + ": range must be > 0");
@@ -490,12 +491,30 @@ void synthesize_packed(const sn_pipeline_config& c, const sn_scene& scene, uint8
         check_direction(r.azimuth, r.elevation);
         const V3 u = unit_vector(r.azimuth, r.elevation);
         const double round_trip = 2.0 * r.range / c.speed_of_sound;
+        e.amplitude.push_back(amplitude);
         for (int ch = 0; ch < kCh; ++ch) {
             const double arrival = round_trip - dot(mic(c, ch), u) / c.speed_of_sound;
             const long onset = std::lround(arrival * c.pdm_rate);
-            if (onset + ref_len > static_cast<int64_t>(n)) {
+            if (onset + ref_len > static_cast<int64_t>(s.frames)) {
                 argument_error("reflector " + std::to_string(k) + ": echo ends past the capture window");
             }
+            e.onset.push_back((int64_t)onset);
+        }
+    }
+    return e;
+}
+
+void synthesize_packed(const sn_pipeline_config& c, const sn_scene& scene, uint8_t* out) {
+    // synth.cpp:116-134 = synthesize_scene (:11-61) -> sigma_delta (:63-94) -> pack (:96-114)
+    const SceneEchoes e = scene_echoes(c, scene);
+    const uint64_t n = e.frames;
+    const std::vector<double>& pulse = e.pulse;
+    const auto ref_len = static_cast<int64_t>(pulse.size());
+    std::vector<double> x(static_cast<size_t>(kCh) * n, 0.0);
+    for (size_t k = 0; k < e.amplitude.size(); ++k) {
+        const double amplitude = e.amplitude[k];
+        for (int ch = 0; ch < kCh; ++ch) {
+            const long onset = (long)e.onset[k * kCh + ch];
             double* dst = x.data() + static_cast<size_t>(ch) * n;
             for (long i = std::max<long>(0, onset); i < onset + ref_len; ++i) {
                 dst[i] += amplitude * pulse[static_cast<size_t>(i - onset)];

@@ -72,6 +72,15 @@ std::vector<double> direction_grid(int kind); // n x (az, el)
 void default_config(int kind, sn_pipeline_config* cfg);
 
 // synth.cpp:116-134: packed bytes of one capture (frame-major, MSB first).
+// Echo geometry of one synthetic scene (synth.cpp:11-61): the pulse at the
+// PDM rate, per reflector its amplitude and per channel its onset sample.
+struct SceneEchoes {
+    uint64_t frames = 0;
+    std::vector<double> pulse;
+    std::vector<double> amplitude;   // [reflector]
+    std::vector<int64_t> onset;      // [reflector][32]
+};
+SceneEchoes scene_echoes(const sn_pipeline_config& c, const sn_scene& scene);
 void synthesize_packed(const sn_pipeline_config& cfg, const sn_scene& scene, uint8_t* out);
 
 } // namespace snb

@@ -1225,6 +1225,55 @@ sn_status sn_workspace_process_frames(sn_workspace* ws, const uint8_t* const* fr
     });
 }
 
+sn_status sn_synthesize_device(const sn_pipeline_config* cfg, const sn_scene* scenes, uint64_t count, int device,
+                               uint8_t* d_packed, void* stream) {
+    return guarded([&] {
+        if (!cfg || (!scenes && count) || (!d_packed && count)) argument_error("null argument");
+        if (device < 0) argument_error("device must be >= 0");
+        if (count == 0) return;
+        std::vector<SynthScene> sc(count);
+        std::vector<double> pulse;
+        uint64_t frames = 0;
+        for (uint64_t i = 0; i < count; ++i) {
+            const SceneEchoes e = scene_echoes(*cfg, scenes[i]);
+            if (e.amplitude.size() > (size_t)kSynthMaxReflectors)
+                argument_error("synthesize_device: more than 8 reflectors in a scene");
+            if (i == 0) {
+                pulse = e.pulse;
+                frames = e.frames;
+            }
+            SynthScene& s = sc[i];
+            s = SynthScene{};
+            s.seed = scenes[i].seed;
+            s.noise_rms = scenes[i].noise_rms;
+            s.n_refl = (int)e.amplitude.size();
+            for (int k = 0; k < s.n_refl; ++k) {
+                s.amp[k] = e.amplitude[k];
+                for (int ch = 0; ch < kCh; ++ch) s.onset[k][ch] = e.onset[(size_t)k * kCh + ch];
+            }
+        }
+        DeviceGuard g(device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int64_t nwords = (int64_t)((frames + 31) / 32);
+        double* d_pulse = nullptr;
+        SynthScene* d_sc = nullptr;
+        uint32_t* d_words = nullptr;
+        ck(cudaMallocAsync(&d_pulse, pulse.size() * sizeof(double), st), "cudaMallocAsync");
+        ck(cudaMallocAsync(&d_sc, count * sizeof(SynthScene), st), "cudaMallocAsync");
+        ck(cudaMallocAsync(&d_words, count * 32 * nwords * sizeof(uint32_t), st), "cudaMallocAsync");
+        ck(cudaMemcpyAsync(d_pulse, pulse.data(), pulse.size() * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(d_sc, sc.data(), count * sizeof(SynthScene), cudaMemcpyHostToDevice, st), "H2D");
+        SynthArgs a{d_pulse, d_sc, d_words, d_packed, (int64_t)frames, (int64_t)pulse.size(), nwords,
+                    (int64_t)(kCh * frames / 8), (int)count};
+        launch_synth(a, st);
+        ck(cudaGetLastError(), "synth launch");
+        cudaFreeAsync(d_pulse, st);
+        cudaFreeAsync(d_sc, st);
+        cudaFreeAsync(d_words, st);
+        ck(cudaStreamSynchronize(st), "synth sync");
+    });
+}
+
 sn_status sn_measure_fp_peak(int device, int precision, double* tflops) {
     return guarded([&] {
         if (!tflops) argument_error("null argument");

@@ -405,3 +405,23 @@ def test_tensor_core_beamformer_scale_invariance(gpu):
     assert np.array_equal(both[0].energies, ws1.process(loud).energies)
     assert np.array_equal(both[1].energies, ws1.process(quiet).energies)
     assert np.isfinite(both[1].energies).all() and both[1].energies.max() < both[0].energies.max()
+
+
+# ---------------------------------------------------------------------------
+# GPU load generator against the host restatement
+# (itself bit-exact with the reference's synthesize_measurement)
+@pytest.mark.parametrize("name", ["tiny", "h90"])
+def test_gpu_synthesis_matches_host(gpu, name):
+    import torch
+    sn = gpu
+    cfg = cfg_for(sn, name)
+    scenes = [sn.Scene([sn.Reflector(0.6 + 0.1 * i, 0.3 - 0.1 * i, 0.05 * i, 0.8),
+                        sn.Reflector(1.0 + 0.05 * i, -0.2, 0.0, 0.4)][: 1 + i % 2], 0.01 * (i % 3), 11 + i)
+              for i in range(5)]
+    nbytes = 32 * cfg.frames() // 8
+    d = torch.zeros(len(scenes) * nbytes, dtype=torch.uint8, device="cuda")
+    sn.synthesize_device(cfg, scenes, d.data_ptr(), device=0)
+    got = d.cpu().numpy().reshape(len(scenes), nbytes)
+    for i, sc in enumerate(scenes):
+        want = sn.synthesize_measurement(cfg, sc).packed
+        assert np.array_equal(got[i], want), f"scene {i}: {int((got[i] != want).sum())} bytes differ"
