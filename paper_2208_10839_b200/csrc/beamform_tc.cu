@@ -116,6 +116,12 @@ __device__ __forceinline__ double i64_ldexp_exact(long long Y, int e) {
     return m ? __longlong_as_double((long long)bits) : 0.0;
 }
 
+// 256-bit global store (STG.E.256 on sm_100): half the store instructions of
+// the epilogue (its global store queue throttled at 128-bit stores)
+__device__ __forceinline__ void st_global_v4(double* p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 // block-floating-point exponent of a capture: max|x| < 2^k
 __device__ __forceinline__ int bfp_exponent(unsigned long long amax_bits) {
     const int ef = (int)((amax_bits >> 52) & 0x7FF);
@@ -376,7 +382,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
                     double* out = reinterpret_cast<double*>(a.beams) + ((size_t)b * a.n_dirs + slot) * a.N + n0;
                     if (n0 + 8 <= a.L) {
 #pragma unroll
-                        for (int i = 0; i < 8; i += 2) *reinterpret_cast<double2*>(out + i) = make_double2(v[i], v[i + 1]);
+                        for (int i = 0; i < 8; i += 4) st_global_v4(out + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
                     } else {
                         for (int i = 0; i < 8; ++i)
                             if (n0 + i < a.L) out[i] = v[i];
