@@ -146,7 +146,7 @@ constexpr int kABytes = 2 * kTcM * 16; // one shift: two channel halves x 128 ro
 __global__ void __launch_bounds__(128) k_digits(DigitArgs a) {
     const int c = blockIdx.y, b = blockIdx.z;
     const int nblk = (a.rows + 127) / 128;
-    const int h = blockIdx.x / nblk;
+    const int h = blockIdx.x / nblk; // channel half
     const int row = (blockIdx.x % nblk) * 128 + threadIdx.x;
     if (row >= a.rows) return;
     // power-of-two scale 2^(46 - k), max|x| < 2^k: exact, and the epilogue
@@ -163,7 +163,9 @@ __global__ void __launch_bounds__(128) k_digits(DigitArgs a) {
     for (int l = 0; l < 16; ++l) {
         const int64_t tp = t - base[l];
         const double x = (tp >= 0 && tp < a.L) ? fb[(size_t)l * a.Lp + tp] : 0.0;
-        long long X = __double2ll_rn(x * inv);
+        // round-to-nearest-even of x 2^(46-k) (|.| <= 2^46) by the magic-number
+        // addition on the FP64 pipe (the F2I.S64.F64 conversion is a slow path)
+        long long X = __double_as_longlong(__dadd_rn(__dmul_rn(x, inv), 6755399441055744.0)) - 0x4338000000000000LL;
 #pragma unroll
         for (int j = 0; j < kTcSlices; ++j) {
             const int d = (int)((X + 128) & 255) - 128; // balanced digit in [-128, 127]
