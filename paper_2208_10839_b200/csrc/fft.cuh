@@ -300,4 +300,32 @@ __device__ __forceinline__ void real_spectral_op(V* buf, int M, const TW& tw, Op
     gsync();
 }
 
+// real_spectral_op specialised to the Hilbert operator of pipeline.cpp:456-459
+// (Y[k] = -i s X[k], DC and Nyquist zeroed, s = 2/N the inverse scaling).
+// Substituting the operator into split -> op -> merge collapses to
+//   Z'[k]   = s (cos t_k conj(Z[M-k]) + i sin t_k Z[k]),
+//   Z'[M-k] = s (i sin t_k Z[M-k] - cos t_k conj(Z[k])),   t_k = 2 pi k / N,
+// one twiddle and 4 multiply-adds per bin pair instead of ~50 operations
+// (s is a power of two, so folding it into the twiddle is exact).
+template <typename V, typename TW, typename R>
+__device__ __forceinline__ void hilbert_spectral(V* buf, int M, const TW& tw, R s) {
+    for (int k = gtid(); k < M / 2; k += kGroupThreads) {
+        if (k == 0) {
+            buf[0] = V{(R)0, (R)0}; // DC and Nyquist (packed in Z[0]) zeroed
+            const V z = buf[pad16(M / 2)];
+            const V w = tw.h(M / 2);
+            const R c = s * w.x, sn = -s * w.y;
+            buf[pad16(M / 2)] = V{c * z.x - sn * z.y, sn * z.x - c * z.y};
+            continue;
+        }
+        const int kk = M - k;
+        const V zk = buf[pad16(k)], zkk = buf[pad16(kk)];
+        const V w = tw.h(k); // (cos t_k, -sin t_k)
+        const R c = s * w.x, sn = -s * w.y;
+        buf[pad16(k)] = V{c * zkk.x - sn * zk.y, sn * zk.x - c * zkk.y};
+        buf[pad16(kk)] = V{-c * zk.x - sn * zkk.y, c * zk.y + sn * zkk.x};
+    }
+    gsync();
+}
+
 } // namespace snb

@@ -435,10 +435,14 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
         }
 #endif
         cfft<M, false, false>(reinterpret_cast<const V*>(src), bufB, twsrc);
+#ifdef SNB_GENERIC_HILBERT
         real_spectral_op(bufB, M, twsrc, [&](V X, int k) {
             if (k == 0 || k == M) return V{(R)0, (R)0};
             return V{X.y * scale, -X.x * scale}; // -i X, with the 2/N of the inverse
         });
+#else
+        hilbert_spectral(bufB, M, twsrc, scale);
+#endif
         cfft<M, true, true>(bufB, bufB, twsrc);
         // |b + iH(b)|: h from the inverse FFT (shared), b re-read from the beam
         // buffer; values kept in registers across the barrier, then written in
