@@ -15,6 +15,8 @@
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 namespace snb {
 
 template <typename R> struct Cx;
@@ -174,8 +176,17 @@ template <typename V> struct TwShared {
 // before a CTA barrier, then stores. M / RADIX butterflies over kGroupThreads
 // threads: BPT = ceil(M / RADIX / kGroupThreads) per thread (1 up to M = 4096
 // with radix 16, 2 for M = 8192).
-template <int RADIX, bool INV, bool SRC_PADDED, int M, typename V, typename TW>
-__device__ __forceinline__ void stockham_pass(const V* src, V* dst, int ns, const TW& tw) {
+// Sink: the last pass of a transform may hand its outputs (index, value) to a
+// consumer instead of storing them (the consumer runs after the pre-store
+// barrier, so it may overwrite the buffer; no trailing barrier).
+struct NoSink {
+    template <typename V> __device__ __forceinline__ void operator()(int, V) const {}
+};
+
+template <int RADIX, bool INV, bool SRC_PADDED, int M, typename V, typename TW, typename Sink = NoSink>
+__device__ __forceinline__ void stockham_pass(const V* src, V* dst, int ns, const TW& tw, Sink sink = {}) {
+    constexpr bool kSink = !std::is_same<Sink, NoSink>::value;
+    static_assert(!kSink || SRC_PADDED, "a sink pass runs in place");
     // SRC_PADDED: in place in the shared buffer, so every thread's loads must
     // finish before any store (barrier below). Otherwise src is a different
     // (global) array and dst is free (callers end their previous use of the
@@ -230,23 +241,29 @@ __device__ __forceinline__ void stockham_pass(const V* src, V* dst, int ns, cons
             const int k = j % ns;
             const int base = (j / ns) * ns * RADIX + k;
 #pragma unroll
-            for (int r = 0; r < RADIX; ++r) dst[pad16(base + out_slot<RADIX>(r) * ns)] = v[bt][r];
+            for (int r = 0; r < RADIX; ++r) {
+                if constexpr (kSink) sink(base + out_slot<RADIX>(r) * ns, v[bt][r]);
+                else dst[pad16(base + out_slot<RADIX>(r) * ns)] = v[bt][r];
+            }
         }
     }
-    gsync();
+    if constexpr (!kSink) gsync();
 }
 
 // Full M-point complex FFT, M a compile-time power of two in [16, 8192]:
 // radix-16 passes, then one radix-2/4/8 pass for the remaining factor. The
 // first pass reads `src` (padded or not); later passes work in place on `buf`.
-template <int M, bool INV, bool SRC_PADDED, int NS = 1, typename V, typename TW>
-__device__ __forceinline__ void cfft(const V* src, V* buf, const TW& tw) {
+// With a sink, the last pass hands its outputs to it (see stockham_pass).
+template <int M, bool INV, bool SRC_PADDED, int NS = 1, typename V, typename TW, typename Sink = NoSink>
+__device__ __forceinline__ void cfft(const V* src, V* buf, const TW& tw, Sink sink = {}) {
     constexpr int REM = M / NS;
-    if constexpr (REM >= 16) {
+    if constexpr (REM == 16) {
+        stockham_pass<16, INV, SRC_PADDED, M>(src, buf, NS, tw, sink);
+    } else if constexpr (REM > 16) {
         stockham_pass<16, INV, SRC_PADDED, M>(src, buf, NS, tw);
-        cfft<M, INV, true, NS * 16>(buf, buf, tw);
+        cfft<M, INV, true, NS * 16>(buf, buf, tw, sink);
     } else if constexpr (REM > 1) {
-        stockham_pass<REM, INV, SRC_PADDED, M>(src, buf, NS, tw);
+        stockham_pass<REM, INV, SRC_PADDED, M>(src, buf, NS, tw, sink);
     }
 }
 

@@ -435,61 +435,30 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
         }
 #endif
         cfft<M, false, false>(reinterpret_cast<const V*>(src), bufB, twsrc);
-#ifdef SNB_GENERIC_HILBERT
-        real_spectral_op(bufB, M, twsrc, [&](V X, int k) {
-            if (k == 0 || k == M) return V{(R)0, (R)0};
-            return V{X.y * scale, -X.x * scale}; // -i X, with the 2/N of the inverse
-        });
-#else
         hilbert_spectral(bufB, M, twsrc, scale);
-#endif
-        cfft<M, true, true>(bufB, bufB, twsrc);
-        // |b + iH(b)|: h from the inverse FFT (shared), b re-read from the beam
-        // buffer; values kept in registers across the barrier, then written in
-        // the decimation-phase layout e_p[u] = env[u*D - c0 + p] (zero outside
-        // [0, L)) that the polyphase FIR below reads with unit stride.
-        constexpr int NV = (2 * M + kGroupThreads - 1) / kGroupThreads;
-        R ev[NV];
-        // all beam loads first (one batch of independent L2 reads), then the
-        // shared Hilbert values and the roots, in place in the same registers
-        // branch-free when NV * kGroupThreads == N: every n < N is a valid
-        // beam (tail zero) and FFT-buffer index; values for n >= L are computed
-        // and never stored
-        constexpr bool kFull = NV * kGroupThreads == 2 * M;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int n = tid + i * kGroupThreads;
-            ev[i] = (kFull || n < 2 * M) ? __ldg(src + n) : (R)0;
-        }
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int n = tid + i * kGroupThreads;
-            if (kFull || n < 2 * M) {
-                const R h = env[n + 2 * (n >> 5)];
-                ev[i] = fast_sqrt(ev[i] * ev[i] + h * h);
-            }
-        }
-        gsync();
-        R* ph = env; // phases: D rows of U entries
+        R* ph = env; // phases: D rows of phase_len entries
         {
-            // t = n + c0 -> slot (t mod D) * phase_len + t / D, stepped by
-            // kGroupThreads samples without division
+            // Inverse transform whose last pass feeds |b + iH(b)| straight into
+            // the decimation-phase layout e_p[u] = env[u*D - c0 + p] (zero outside
+            // [0, L)) that the polyphase FIR reads with unit stride: output n of
+            // the last pass is the pair h[2n], h[2n+1]; b[2n], b[2n+1] come from
+            // the beam buffer (one 16-byte load). Slot of sample t = n + c0:
+            // (t mod D) * phase_len + t / D, t / D by a multiply-high.
             const int D = a.decim, PL = a.phase_len;
-            const int du = kGroupThreads / D, dp = kGroupThreads - du * D;
-            const int t0 = tid + c0;
-            int pp = t0 % D;
-            int addr = pp * PL + t0 / D;
-            const int step = du + dp * PL, wrap = 1 - D * PL;
-#pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                if (tid + i * kGroupThreads < L) ph[addr] = ev[i];
-                addr += step;
-                pp += dp;
-                if (pp >= D) {
-                    pp -= D;
-                    addr += wrap;
-                }
-            }
+            const unsigned dmagic = 0xffffffffu / (unsigned)D + 1u; // exact for t < 2^32 / D
+            const V* bsrc = reinterpret_cast<const V*>(src);
+            const int Li = (int)L;
+            auto sink = [&](int n, V h) {
+                const V bv = __ldg(bsrc + n);
+                const R m0 = fast_sqrt(bv.x * bv.x + h.x * h.x);
+                const R m1 = fast_sqrt(bv.y * bv.y + h.y * h.y);
+                const unsigned t = 2u * (unsigned)n + (unsigned)c0;
+                const int u = (int)__umulhi(t, dmagic);
+                const int pp = (int)t - u * D;
+                if (2 * n < Li) ph[pp * PL + u] = m0;
+                if (2 * n + 1 < Li) ph[pp + 1 == D ? u + 1 : (pp + 1) * PL + u] = m1;
+            };
+            cfft<M, true, true>(bufB, bufB, twsrc, sink);
             // zero the slots whose sample lies outside [0, L): per phase row p,
             // u < ceil((c0 - p) / D) and u >= ceil((L + c0 - p) / D)
             if (tid < D) {
