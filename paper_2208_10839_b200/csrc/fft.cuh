@@ -345,4 +345,100 @@ __device__ __forceinline__ void hilbert_spectral(V* buf, int M, const TW& tw, R 
     gsync();
 }
 
+// The middle of the Hilbert transform for M = 4096 (= kGroupThreads radix-16
+// butterflies per pass), entirely in registers: the last forward pass, the
+// Hilbert operator of hilbert_spectral and the first inverse pass, replacing
+// two shared-memory round trips and two barriers with a warp shuffle.
+// Butterfly j of the last forward pass yields Z[j + 256 S], S = 0..15; the
+// complementary bins M - j - 256 S = (256 - j) + 256 (15 - S) all belong to
+// butterfly 256 - j, so butterflies j and 256 - j are placed on lanes l and
+// l + 16 of one warp (j = 0 and j = 128 pair with themselves), exchange with
+// __shfl_xor(16), and each applies the operator to its own 16 bins; those are
+// exactly the inputs of inverse butterfly j (ns = 1). Twiddles of the
+// operator: e^{-i t_k}, t_k = t_j + 2 pi S / 32, by angle addition from one
+// table value per thread.
+__device__ __forceinline__ constexpr double cos_pi16(int k) { // cos(k pi / 16), k in [0, 8]
+    return k == 0 ? 1.0 : k == 1 ? 0.98078528040323044913 : k == 2 ? 0.92387953251128675613
+         : k == 3 ? 0.83146961230254523708 : k == 4 ? 0.70710678118654752440 : k == 5 ? 0.55557023301960222474
+         : k == 6 ? 0.38268343236508977173 : k == 7 ? 0.19509032201612826785 : 0.0;
+}
+template <typename V> __device__ __forceinline__ V shfl_xor16(V v) {
+    return V{__shfl_xor_sync(0xffffffffu, v.x, 16), __shfl_xor_sync(0xffffffffu, v.y, 16)};
+}
+
+template <typename V, typename TW, typename R>
+__device__ __forceinline__ void hilbert_mid_4096(V* buf, const TW& tw, R s) {
+    constexpr int M = 4096, NS = M / 16;
+    static_assert(NS == kGroupThreads, "one butterfly per thread");
+    const int t = gtid(), l = t & 31;
+    const int m = 16 * (t >> 5) + (l & 15);
+    const int j = l < 16 ? m : (m == 0 ? NS / 2 : NS - m);
+    const bool self0 = t == 0, self_half = t == 16; // j = 0, j = 128
+    // last forward pass (radix 16, ns = 256), as stockham_pass
+    V z[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) z[r] = buf[pad16(j + r * NS)];
+    {
+        V w[16];
+        w[1] = tw.w(M, NS, 16, j, 1);
+        w[2] = tw.w(M, NS, 16, j, 2);
+        w[4] = tw.w(M, NS, 16, j, 4);
+        w[8] = tw.w(M, NS, 16, j, 8);
+        w[3] = cmul(w[1], w[2]);
+        w[5] = cmul(w[1], w[4]);
+        w[6] = cmul(w[2], w[4]);
+        w[7] = cmul(w[3], w[4]);
+#pragma unroll
+        for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
+#pragma unroll
+        for (int r = 1; r < 16; ++r) z[r] = cmul(z[r], w[r]);
+    }
+    dft16<false>(z); // z[out_slot(S)] = Z[j + 256 S]
+    const V hj = tw.h(j);
+    const R cj = s * hj.x, sj = -s * hj.y; // s (cos t_j, sin t_j), s a power of two
+    auto cosS = [](int S) { return (R)(S <= 8 ? cos_pi16(S) : -cos_pi16(16 - S)); }; // cos(2 pi S / 32)
+    auto sinS = [](int S) { return (R)cos_pi16(S <= 8 ? 8 - S : S - 8); };
+    // Z'[k] = s (cos t_k conj(Z[M-k]) + i sin t_k Z[k])
+    auto op = [&](V zk, V zc, int S) {
+        const R c = cj * cosS(S) - sj * sinS(S), sn = sj * cosS(S) + cj * sinS(S);
+        return V{c * zc.x - sn * zk.y, sn * zk.x - c * zc.y};
+    };
+#pragma unroll
+    for (int S = 0; S < 8; ++S) {
+        V& a = z[out_slot<16>(S)];
+        V& b = z[out_slot<16>(15 - S)];
+        V pa = shfl_xor16(b), pb = shfl_xor16(a); // partner's Z[15 - S], Z[S]
+        if (self_half) {
+            pa = b;
+            pb = a;
+        }
+        if (!self0) {
+            const V na = op(a, pa, S), nb = op(b, pb, 15 - S);
+            a = na;
+            b = nb;
+        }
+    }
+    if (self0) {
+        // bins 256 S pair with 256 (16 - S); DC and Nyquist (Z[0]) zeroed
+        z[0] = V{(R)0, (R)0};
+#pragma unroll
+        for (int S = 1; S <= 8; ++S) {
+            V& a = z[out_slot<16>(S)];
+            V& b = z[out_slot<16>(16 - S)];
+            const V na = op(a, b, S), nb = op(b, a, 16 - S);
+            a = na;
+            if (S != 8) b = nb;
+        }
+    }
+    // first inverse pass (radix 16, ns = 1): inputs Z'[j + 256 r]
+    V x[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) x[r] = z[out_slot<16>(r)];
+    dft16<true>(x);
+    gsync(); // every thread's forward-pass loads are done
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[pad16(16 * j + out_slot<16>(r))] = x[r];
+    gsync();
+}
+
 } // namespace snb

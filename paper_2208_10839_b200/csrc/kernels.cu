@@ -434,8 +434,14 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
             }
         }
 #endif
-        cfft<M, false, false>(reinterpret_cast<const V*>(src), bufB, twsrc);
-        hilbert_spectral(bufB, M, twsrc, scale);
+        if constexpr (M == 4096) {
+            stockham_pass<16, false, false, M>(reinterpret_cast<const V*>(src), bufB, 1, twsrc);
+            stockham_pass<16, false, true, M>(bufB, bufB, 16, twsrc);
+            hilbert_mid_4096(bufB, twsrc, scale);
+        } else {
+            cfft<M, false, false>(reinterpret_cast<const V*>(src), bufB, twsrc);
+            hilbert_spectral(bufB, M, twsrc, scale);
+        }
         R* ph = env; // phases: D rows of phase_len entries
         {
             // Inverse transform whose last pass feeds |b + iH(b)| straight into
@@ -458,7 +464,12 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
                 if (2 * n < Li) ph[pp * PL + u] = m0;
                 if (2 * n + 1 < Li) ph[pp + 1 == D ? u + 1 : (pp + 1) * PL + u] = m1;
             };
-            cfft<M, true, true>(bufB, bufB, twsrc, sink);
+            if constexpr (M == 4096) {
+                stockham_pass<16, true, true, M>(bufB, bufB, 16, twsrc);
+                stockham_pass<16, true, true, M>(bufB, bufB, 256, twsrc, sink);
+            } else {
+                cfft<M, true, true>(bufB, bufB, twsrc, sink);
+            }
             // zero the slots whose sample lies outside [0, L): per phase row p,
             // u < ceil((c0 - p) / D) and u >= ceil((L + c0 - p) / D)
             if (tid < D) {
