@@ -441,4 +441,17 @@ __device__ __forceinline__ void hilbert_mid_4096(V* buf, const TW& tw, R s) {
     gsync();
 }
 
+// First pass (radix 16, ns = 1) of an M = 16 * kGroupThreads transform from
+// inputs already in registers (v[r] = x[gtid() + r * M / 16]), so that the
+// caller can issue the global loads early (e.g. before the previous item's
+// tail work).
+template <bool INV, typename V>
+__device__ __forceinline__ void first_pass_from_regs(V (&v)[16], V* dst) {
+    dft16<INV>(v);
+    const int base = 16 * gtid();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) dst[pad16(base + out_slot<16>(r))] = v[r];
+    gsync();
+}
+
 } // namespace snb

@@ -420,6 +420,22 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
     const R scale = (R)2 / (R)N;
     const int c0 = (a.comp_len - 1) / 2;
     R* env = reinterpret_cast<R*>(bufB); // env[n] at n + 2*(n >> 5) (pad16 of the complex view)
+    // M = 4096: the first pass's inputs of the next item are loaded into
+    // registers before the current item's FIR, so their L2 latency hides
+    // behind it
+#ifndef SNB_PRE
+#define SNB_PRE 4
+#endif
+    constexpr int kPre = SNB_PRE; // of the 16 inputs per thread: 4 fit the FP64 register budget (8: spills, slower)
+    V pre[16];
+    auto load_pre = [&](int64_t item) {
+        const V* s = reinterpret_cast<const V*>(a.beams) + (size_t)item * M;
+#pragma unroll
+        for (int r = 0; r < kPre; ++r) pre[r] = __ldg(s + tid + r * kGroupThreads);
+    };
+    if constexpr (M == 4096) {
+        if ((int64_t)blockIdx.x * G + grp < items) load_pre((int64_t)blockIdx.x * G + grp);
+    }
     for (int64_t it = (int64_t)blockIdx.x * G + grp; it < items; it += (int64_t)gridDim.x * G) {
         const int64_t b = it / a.n_dirs, slot = it % a.n_dirs;
         const R* src = reinterpret_cast<const R*>(a.beams) + (size_t)it * N;
@@ -435,7 +451,9 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
         }
 #endif
         if constexpr (M == 4096) {
-            stockham_pass<16, false, false, M>(reinterpret_cast<const V*>(src), bufB, 1, twsrc);
+#pragma unroll
+            for (int r = kPre; r < 16; ++r) pre[r] = __ldg(reinterpret_cast<const V*>(src) + tid + r * kGroupThreads);
+            first_pass_from_regs<false>(pre, bufB);
             stockham_pass<16, false, true, M>(bufB, bufB, 16, twsrc);
             hilbert_mid_4096(bufB, twsrc, scale);
         } else {
@@ -480,6 +498,10 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
                 for (int k = 0; k < lo; ++k) row[k] = 0;
                 for (int k = hi; k < a.phase_len; ++k) row[k] = 0;
             }
+        }
+        if constexpr (M == 4096) {
+            const int64_t nx = it + (int64_t)gridDim.x * G;
+            if (nx < items) load_pre(nx);
         }
         gsync();
         float* eo = a.energy + ((size_t)b * a.n_dirs + a.order[slot]) * a.bins;
