@@ -313,28 +313,37 @@ __device__ __forceinline__ float fast_sqrt(float x) { return sqrtf(x); }
 //
 // Fast path (D = 10, Q = 45): warps 0-3 of the group sum phases 0-4, warps 4-7
 // phases 5-9, for the same kFirR consecutive outputs per thread; a register
-// window slides over the row (one LDS per kFirR FMAs, conflict-free for odd
-// kFirR) and every tap is a compile-time index into the kernel-parameter
-// array, i.e. a constant-bank operand of the FMA. The upper half hands its
-// partial sums to the lower half through `red`.
+// window slides over the row, refilled two samples per 16-byte load, and the
+// taps (warp-uniform: broadcast) come two per load; the phase loop is rolled
+// (the fully unrolled form overflowed the instruction cache). The upper half
+// hands its partial sums to the lower half through `red`.
 template <int H, typename R>
 __device__ __forceinline__ void fir_half(const R* ph, int phase_len, int k0, R (&acc)[kFirR], const R* staps) {
-    // taps from shared memory (phase-major, warp-uniform address: broadcast),
-    // phase loop rolled: ~400 instructions of code; the fully unrolled
-    // 10-phase form with constant-bank taps overflowed the instruction cache
-    // (measured 2.6% slower)
+    using V = typename Cx<R>::T;
     constexpr int P0 = H * (kFirD / 2);
 #pragma unroll 1
     for (int pp = 0; pp < kFirD / 2; ++pp) {
-        const R* row = ph + (P0 + pp) * phase_len + k0;
-        const R* tp = staps + (P0 + pp) * kFirQ;
-        R w[kFirR + kFirQ];
+        const V* row = reinterpret_cast<const V*>(ph + (P0 + pp) * phase_len + k0);
+        const V* tp = reinterpret_cast<const V*>(staps + (P0 + pp) * kFirQP);
+        R w[kFirR + kFirQ + 1];
 #pragma unroll
-        for (int r = 0; r < kFirR; ++r) w[r] = row[r];
+        for (int r = 0; r < kFirR / 2; ++r) {
+            const V v = row[r];
+            w[2 * r] = v.x;
+            w[2 * r + 1] = v.y;
+        }
+        V c2;
 #pragma unroll
         for (int q = 0; q < kFirQ; ++q) {
-            if (q + 1 < kFirQ) w[kFirR + q] = row[kFirR + q]; // used from step q + 1 on
-            const R c = tp[q];
+            if ((q & 1) == 0) {
+                if (q + 2 < kFirQ) { // w[kFirR + q], w[kFirR + q + 1]: used from step q + 1 on
+                    const V v = row[(kFirR + q) / 2];
+                    w[kFirR + q] = v.x;
+                    w[kFirR + q + 1] = v.y;
+                }
+                c2 = tp[q / 2];
+            }
+            const R c = (q & 1) ? c2.y : c2.x;
 #pragma unroll
             for (int r = 0; r < kFirR; ++r) acc[r] = fma(c, w[q + r], acc[r]);
         }

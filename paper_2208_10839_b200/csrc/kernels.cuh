@@ -79,14 +79,18 @@ struct EnvArgs {
 
 // Polyphase smoothing FIR fast path (the reference's default composite
 // filter: 447 taps at stride 10 -> 10 phases x 45 taps): every thread owns
-// kFirR consecutive outputs (odd: bank-conflict free) over one half of the
-// phases; the phase-major taps travel in the kernel parameters and are copied
-// to shared memory once per CTA.
-constexpr int kFirR = 7;
+// kFirR consecutive outputs over one half of the phases; kFirR = 2 mod 4 so
+// that the row window and the taps are read as 16-byte pairs without bank
+// conflicts (lane stride kFirR / 2 = odd 16-byte chunks). The phase-major
+// taps (kFirQP per phase, zero-padded to even) travel in the kernel
+// parameters and are copied to shared memory once per CTA.
+constexpr int kFirR = 6;
 constexpr int kFirD = 10, kFirQ = 45;              // decimation, taps per phase
-constexpr int kFirTaps = kFirD * kFirQ;            // 450 (zero-padded)
+constexpr int kFirQP = kFirQ + 1;                  // taps per phase, padded to even
+constexpr int kFirTaps = kFirD * kFirQP;           // 460 (zero-padded)
 constexpr int kFirScratch = 128 * kFirR;           // half-sum exchange (reals)
-template <typename R> struct FirTaps { R c[kFirTaps]; }; // c[p * kFirQ + q] = comp[q * kFirD + p]
+static_assert(kFirR % 4 == 2, "paired conflict-free loads");
+template <typename R> struct FirTaps { R c[kFirTaps]; }; // c[p * kFirQP + q] = comp[q * kFirD + p]
 constexpr int kEnvGroupsF64 = 1;
 constexpr int kEnvGroupsF32 = 1;
 

@@ -370,16 +370,17 @@ struct sn_workspace {
             const int c0 = (int)(plan.comp_rev.size() - 1) / 2;
             fir_q = (int)((plan.comp_rev.size() + D - 1) / D);
             const int groups = (int)((s.bins + kFirR - 1) / kFirR);
-            phase_len = std::max(groups * kFirR + fir_q, (int)((s.mf_len + c0) / D) + 1);
+            phase_len = std::max(groups * kFirR + fir_q + 1, (int)((s.mf_len + c0) / D) + 1);
             phase_len = std::max(phase_len, (int)s.bins + fir_q + 1);
+            phase_len = (phase_len + 1) & ~1; // even: rows stay 16-byte aligned (paired loads)
             fir_fast = D == kFirD && fir_q == kFirQ && groups <= 128;
             if (fir_fast) {
                 for (int p = 0; p < kFirD; ++p) {
                     for (int q = 0; q < kFirQ; ++q) {
                         const size_t j = (size_t)q * kFirD + p;
                         const double v = j < plan.comp_rev.size() ? plan.comp_rev[j] : 0.0;
-                        taps64.c[p * kFirQ + q] = v;
-                        taps32.c[p * kFirQ + q] = (float)v;
+                        taps64.c[p * kFirQP + q] = v;
+                        taps32.c[p * kFirQP + q] = (float)v;
                     }
                 }
             }
