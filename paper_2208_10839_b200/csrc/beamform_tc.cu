@@ -139,9 +139,37 @@ constexpr int kABytes = 2 * kTcM * 16; // one shift: two channel halves x 128 ro
 } // namespace
 
 // ---------------------------------------------------------------------------
-// k_digits: filt (FP64) -> per-cluster re-centred digit planes.
+// k_digit_words: filt (FP64) -> the six balanced base-256 digits of every
+// sample, once per (capture, channel, sample): X = round(x * 2^(46 - k)),
+// max|x| < 2^k (power-of-two scale: exact; the epilogue rescales by an
+// exponent add), X = sum_j 256^j d_j, d_j in [-128, 127], byte j of the word =
+// d_j & 255.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_digit_words(DigitArgs a) {
+    const int ch = blockIdx.y, b = blockIdx.z;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.L) return;
+    const int kexp = bfp_exponent(a.amax_bits[b]);
+    const double inv = __longlong_as_double((long long)(46 - kexp + 1023) << 52);
+    const double x = a.filt[((size_t)b * 32 + ch) * a.Lp + a.H + t];
+    // round-to-nearest-even of x 2^(46-k) (|.| <= 2^46) by the magic-number
+    // addition on the FP64 pipe (the F2I.S64.F64 conversion is a slow path)
+    long long X = __double_as_longlong(__dadd_rn(__dmul_rn(x, inv), 6755399441055744.0)) - 0x4338000000000000LL;
+    uint32_t w[2] = {0u, 0u};
+#pragma unroll
+    for (int j = 0; j < kTcSlices; ++j) {
+        const int d = (int)((X + 128) & 255) - 128; // balanced digit in [-128, 127]
+        X = (X - d) >> 8;
+        w[j >> 2] |= (uint32_t)(d & 255) << (8 * (j & 3));
+    }
+    a.words[((size_t)b * 32 + ch) * a.L + t] = make_uint2(w[0], w[1]);
+}
+
+// ---------------------------------------------------------------------------
+// k_digits: digit words -> per-cluster re-centred digit planes.
 // planes[((b * C + c) * 12 + 2 j + h) * rows + row][l] = digit j of
-// X_i[row - pad - base[c][i]], i = 16 h + l, X = round(x * 2^46 / max|x|).
+// X_i[row - pad - base[c][i]], i = 16 h + l: a gather of 16 channel words at
+// their cluster shifts and a 4 x 4 byte transpose per 4 channels (PRMT).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_digits(DigitArgs a) {
     const int c = blockIdx.y, b = blockIdx.z;
@@ -149,29 +177,31 @@ __global__ void __launch_bounds__(128) k_digits(DigitArgs a) {
     const int h = blockIdx.x / nblk; // channel half
     const int row = (blockIdx.x % nblk) * 128 + threadIdx.x;
     if (row >= a.rows) return;
-    // power-of-two scale 2^(46 - k), max|x| < 2^k: exact, and the epilogue
-    // rescales by an exponent add
-    const int kexp = bfp_exponent(a.amax_bits[b]);
-    const double inv = __longlong_as_double((long long)(46 - kexp + 1023) << 52);
     const int64_t t = (int64_t)row - a.pad;
-    const double* fb = a.filt + ((size_t)b * 32 + 16 * h) * a.Lp + a.H;
+    const uint2* wb = a.words + ((size_t)b * 32 + 16 * h) * a.L;
     const int32_t* base = a.base + (size_t)c * 32 + 16 * h;
-    uint32_t w[kTcSlices][4];
-#pragma unroll
-    for (int j = 0; j < kTcSlices; ++j) w[j][0] = w[j][1] = w[j][2] = w[j][3] = 0;
+    uint2 d[16];
 #pragma unroll
     for (int l = 0; l < 16; ++l) {
         const int64_t tp = t - base[l];
-        const double x = (tp >= 0 && tp < a.L) ? fb[(size_t)l * a.Lp + tp] : 0.0;
-        // round-to-nearest-even of x 2^(46-k) (|.| <= 2^46) by the magic-number
-        // addition on the FP64 pipe (the F2I.S64.F64 conversion is a slow path)
-        long long X = __double_as_longlong(__dadd_rn(__dmul_rn(x, inv), 6755399441055744.0)) - 0x4338000000000000LL;
+        d[l] = (tp >= 0 && tp < a.L) ? wb[(size_t)l * a.L + tp] : make_uint2(0u, 0u);
+    }
+    uint32_t w[kTcSlices][4];
 #pragma unroll
-        for (int j = 0; j < kTcSlices; ++j) {
-            const int d = (int)((X + 128) & 255) - 128; // balanced digit in [-128, 127]
-            X = (X - d) >> 8;
-            w[j][l >> 2] |= (uint32_t)(d & 255) << (8 * (l & 3));
-        }
+    for (int q = 0; q < 4; ++q) {
+        // plane j, word q: byte k = digit j of channel 4 q + k
+        const uint32_t t0 = __byte_perm(d[4 * q].x, d[4 * q + 1].x, 0x5140);
+        const uint32_t t1 = __byte_perm(d[4 * q].x, d[4 * q + 1].x, 0x7362);
+        const uint32_t t2 = __byte_perm(d[4 * q + 2].x, d[4 * q + 3].x, 0x5140);
+        const uint32_t t3 = __byte_perm(d[4 * q + 2].x, d[4 * q + 3].x, 0x7362);
+        w[0][q] = __byte_perm(t0, t2, 0x5410);
+        w[1][q] = __byte_perm(t0, t2, 0x7632);
+        w[2][q] = __byte_perm(t1, t3, 0x5410);
+        w[3][q] = __byte_perm(t1, t3, 0x7632);
+        const uint32_t t4 = __byte_perm(d[4 * q].y, d[4 * q + 1].y, 0x5140);
+        const uint32_t t5 = __byte_perm(d[4 * q + 2].y, d[4 * q + 3].y, 0x5140);
+        w[4][q] = __byte_perm(t4, t5, 0x5410);
+        w[5][q] = __byte_perm(t4, t5, 0x7632);
     }
     const size_t plane = ((size_t)b * a.clusters + c) * 12;
 #pragma unroll
@@ -407,6 +437,7 @@ size_t beamform_tc_smem_bytes(int rmax, int pad) {
 }
 
 void launch_digits(const DigitArgs& a, int batch, cudaStream_t s) {
+    k_digit_words<<<dim3((unsigned)((a.L + 255) / 256), 32, batch), 256, 0, s>>>(a);
     const int nblk = (a.rows + 127) / 128;
     k_digits<<<dim3(2 * nblk, a.clusters, batch), 128, 0, s>>>(a);
 }

@@ -168,6 +168,7 @@ struct DigitArgs {
     const unsigned long long* amax_bits; // [B]
     const int32_t* base;               // [C][32] per-cluster channel base shift
     int8_t* planes;                    // [B][C][6][2][rows][16]
+    uint2* words;                      // [B][32][L] the 6 digits of each sample, byte j = digit j
     int64_t L, Lp;
     int H, rows, pad, clusters;
 };

@@ -184,6 +184,7 @@ struct sn_workspace {
     int tc_clusters = 0, tc_pad = 0, tc_rows = 0, tc_ntiles = 0, tc_grid = 0;
     std::vector<int32_t> tc_R;
     int8_t* d_planes = nullptr;
+    uint2* d_dwords = nullptr;
     uint8_t* d_resid = nullptr;
     int32_t* d_tc_R = nullptr;
     int32_t* d_tc_start = nullptr;
@@ -222,7 +223,7 @@ struct sn_workspace {
         for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
                         (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot,  (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
-                        (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32, (void*)d_tw_small, (void*)d_tw_small32, (void*)d_planes, (void*)d_resid,
+                        (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32, (void*)d_tw_small, (void*)d_tw_small32, (void*)d_planes, (void*)d_dwords, (void*)d_resid,
                         (void*)d_tc_R, (void*)d_tc_base, (void*)d_amax, (void*)d_tc_start, (void*)d_tc_size,
                         (void*)d_crc_slice, (void*)d_crc_shift, (void*)d_img_tpl, (void*)d_frames_out,
                         (void*)d_frames_in, (void*)d_ids, (void*)d_crc_acc, (void*)d_crc_ok}) {
@@ -521,6 +522,7 @@ struct sn_workspace {
         if (!tc) return;
         uint64_t& n = device_allocs;
         d_planes = dmalloc<int8_t>(max_batch * (uint64_t)tc_clusters * 12 * tc_rows * 16, n);
+        d_dwords = dmalloc<uint2>(max_batch * (uint64_t)kCh * plan.sz.mf_len, n);
         d_resid = dmalloc<uint8_t>(tc_resid.size(), n);
         d_tc_R = dmalloc<int32_t>(tc_R.size(), n);
         d_tc_base = dmalloc<int32_t>(tc_base.size(), n);
@@ -580,7 +582,7 @@ struct sn_workspace {
         launch_matched_filter(ma, (int)count, mf_smem, s);
         if (profiling) cudaEventRecord(ev[3], s);
         if (tc) {
-            DigitArgs dg{d_filt, d_amax, d_tc_base, d_planes, (int64_t)z.mf_len, (int64_t)lp, halo, tc_rows,
+            DigitArgs dg{d_filt, d_amax, d_tc_base, d_planes, d_dwords, (int64_t)z.mf_len, (int64_t)lp, halo, tc_rows,
                          tc_pad, tc_clusters};
             launch_digits(dg, (int)count, s);
             TcArgs ta{};
@@ -620,7 +622,7 @@ struct sn_workspace {
         if (with_envelope) enqueue_envelope(0, count, d_out, s);
         if (profiling) cudaEventRecord(ev[5], s);
         ck(cudaGetLastError(), "kernel launch");
-        last_launches = tc ? 6 : 5;
+        last_launches = tc ? 7 : 5;
     }
 
     // Envelope stage for captures [b0, b0 + count) of the batch whose beams
@@ -722,7 +724,7 @@ struct sn_workspace {
                 off += k;
             }
             ck(cudaGetLastError(), "kernel launch");
-            last_launches = (tc ? 5 : 4) + nch;
+            last_launches = (tc ? 6 : 4) + nch;
             ck(cudaStreamSynchronize(s_d2h), "process sync");
             if (!out_pinned) std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
             done += c;
@@ -1050,7 +1052,7 @@ sn_status sn_workspace_process_device_graph(sn_workspace* ws, const uint8_t* d_p
             ws->g_count = count;
         }
         ck(cudaGraphLaunch(ws->graph, s), "graph launch");
-        ws->last_launches = ws->tc ? 6 : 5;
+        ws->last_launches = ws->tc ? 7 : 5;
     });
 }
 

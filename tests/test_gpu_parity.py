@@ -224,8 +224,9 @@ def test_device_path_and_graph_replay_match_host_path(gpu):
         ws.process_device(dp.data_ptr(), B, out.data_ptr(), s.cuda_stream, graph=True)
     s.synchronize()
     assert np.array_equal(out.cpu().numpy(), host)
-    # demod, pre-MF, matched filter, digit planes, tensor-core delay-and-sum, envelope
-    assert ws.last_launches() == 6
+    # demod, pre-MF, matched filter, digit words, digit planes, tensor-core
+    # delay-and-sum, envelope
+    assert ws.last_launches() == 7
 
 
 def test_decode_errors_on_device_workspace(gpu):
@@ -383,9 +384,9 @@ def test_tensor_core_beamformer_vs_tiled_and_reference(gpu, po, ref, name, monke
     ws_t = sn.Workspace(cfg, device=0)
     monkeypatch.setenv("SNB_BEAMFORMER", "tc")
     ws_c = sn.Workspace(cfg, device=0)
-    assert ws_c.last_launches() in (0, 6)
+    assert ws_c.last_launches() in (0, 7)
     e_t, e_c = ws_t.process(m).energies, ws_c.process(m).energies
-    assert ws_c.last_launches() == 6 and ws_t.last_launches() == 5
+    assert ws_c.last_launches() == 7 and ws_t.last_launches() == 5
     want = ref.workspace(to_oracle(po, cfg)).process(m.packed)
     check_f64(e_c, want)
     check_f64(e_c, e_t)
