@@ -91,8 +91,8 @@ def read_launches(path):
 
 
 def short(name):
-    for k in ("k_demod", "k_premf", "k_matched_filter", "k_beamform_tiles", "k_beamform_tc", "k_digits",
-              "k_envelope", "k_rfft_forward"):
+    for k in ("k_demod", "k_premf", "k_matched_filter", "k_beamform_tiles", "k_beamform_tc", "k_digit_words",
+              "k_digits", "k_envelope", "k_rfft_forward"):
         if k in name:
             return k
     return name.split("(")[0][-40:]
@@ -105,7 +105,7 @@ def main():
     tpath = os.path.join(PROF, "traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     stage_of = {"k_demod": "demod", "k_premf": "premf", "k_matched_filter": "matched_filter",
-                "k_beamform_tiles": "beamform", "k_digits": "beamform", "k_beamform_tc": "beamform",
+                "k_beamform_tiles": "beamform", "k_digit_words": "beamform", "k_digits": "beamform", "k_beamform_tc": "beamform",
                 "k_envelope": "envelope"}
     for i in range(0, len(items), 3):
         rep, launches, key = items[i], items[i + 1], items[i + 2]
