@@ -88,6 +88,22 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const int32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+        "%13, %14, %15, %16};\n" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
@@ -129,7 +145,9 @@ __device__ __forceinline__ int bfp_exponent(unsigned long long amax_bits) {
 }
 
 
-constexpr int kSlots = 512 / kTcN;            // TMEM ring of accumulator slots of kTcN columns
+// TMEM ring of accumulator slots of TN columns: 8 x 64, or 3 x 128 with the
+// last 128 columns the epilogue's scratch (Y_hi parked between planes)
+template <int TN> constexpr int slots_for() { return TN == 64 ? 8 : TN == 96 ? 5 : 3; }
 constexpr int kWin = 3;                       // B window buffers (loads run kWin - 1 tiles ahead)
 constexpr int kEpiWarps = 16;                  // epilogue warps; warp 8 produces and issues
 constexpr int kTcThreads = 32 * (kEpiWarps + 1);
@@ -239,10 +257,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
+template <int TN>
 __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const __grid_constant__ TcSched sched) {
+    constexpr int kSlots = slots_for<TN>();
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int wrows = kTcN + a.pad;                     // window rows per (digit, half)
+    const int wrows = TN + a.pad;                       // window rows per (digit, half)
     const size_t bbuf = (size_t)12 * wrows * 16;        // one B window set
     uint8_t* Ares = smem;                               // [rmax][2][128][16]
     uint8_t* Bw = smem + (size_t)a.rmax * kABytes;      // [kWin][12][wrows][16]
@@ -273,7 +293,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
 
     if (warp == kEpiWarps) {
         // ===================== producer / MMA issuer warp =====================
-        const uint32_t idesc = idesc_i8(kTcM, kTcN);
+        const uint32_t idesc = idesc_i8(kTcM, TN);
         const uint32_t ares_addr = su32(Ares), bw_addr = su32(Bw);
         const bool leader = elect_one();
         auto load_window = [&](int g) {
@@ -281,9 +301,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
             const int c = t / per_cb, rem = t - c * per_cb;
             const int b = rem / a.ntiles, tt = rem - b * a.ntiles;
             const int R = a.R[c];
-            const uint32_t bytes = (uint32_t)(kTcN + R - 1) * 16;
+            const uint32_t bytes = (uint32_t)(TN + R - 1) * 16;
             const int8_t* pb = a.planes +
-                (((size_t)b * a.clusters + c) * 12 * a.rows + (size_t)(a.pad + tt * kTcN - (R - 1))) * 16;
+                (((size_t)b * a.clusters + c) * 12 * a.rows + (size_t)(a.pad + tt * TN - (R - 1))) * 16;
             uint8_t* dst = Bw + (size_t)(g % kWin) * bbuf;
             if (leader) {
                 mbar_expect_tx(&wfull[g % kWin], 12 * bytes);
@@ -344,7 +364,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
                 if (leader) {
                     uint64_t ad = a0;
                     uint64_t bd = b0 + (uint64_t)(2 * wrows * j); // plane j, 16-byte units
-                    const uint32_t tacc = tmem + (uint32_t)(sl * kTcN);
+                    const uint32_t tacc = tmem + (uint32_t)(sl * TN);
                     for (int r = 0; r < R; ++r) {
                         mma_i8(tacc, ad, bd, idesc, r > 0 ? 1u : 0u);
                         ad += (uint64_t)(kABytes >> 4);
@@ -362,8 +382,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
         // warp w: TMEM lane quarter w & 3 (directions), column quarter w >> 2
         const int quarter = warp & 3, colq = warp >> 2;
         const int d = quarter * 32 + lane;
-        constexpr int NC = kTcN / 4; // columns per thread
-        static_assert(NC == 16, "epilogue column chunk: one 32x32b.x16 TMEM load");
+        constexpr int NC = TN / 4; // columns per thread
+        constexpr bool kPark = TN == 128; // Y_hi parked in TMEM scratch columns (register budget)
+        static_assert(NC % 8 == 0 && (!kPark || NC == 32), "epilogue column chunks");
+        const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+        const uint32_t scratch = tmem + lane_base + (uint32_t)(kSlots * TN + colq * NC); // kPark only
         for (int g = 0; g < ntile; ++g) {
             const int t = t_beg + g;
             const int c = t / per_cb, rem = t - c * per_cb;
@@ -371,53 +394,97 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
             const bool live = d < __ldg(a.cl_size + c);
             const int64_t slot = (int64_t)__ldg(a.cl_start + c) + d;
             const int eadj = bfp_exponent(__ldg(a.amax_bits + b)) - 46 - 5; // beam = Y 2^(k - 46) / 32
-            int32_t yh[NC], yl[NC];
+            // planes 5, 4, 3 -> Y_hi; 2, 1, 0 -> Y_lo (|.| < 2^29, exact in int32)
+            int32_t yh[kPark ? 1 : NC], yl[NC];
 #pragma unroll
             for (int p = 0; p < kTcSlices; ++p) {
                 const int q = kTcSlices * g + p, sl = q % kSlots;
                 mbar_wait(&sfull[sl], (uint32_t)((q / kSlots) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                uint32_t y[NC];
-                tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sl * kTcN + colq * NC), y);
-                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sempty[sl]);
-                // planes 5, 4, 3 -> Y_hi; 2, 1, 0 -> Y_lo (|.| < 2^29, exact in int32)
+                const uint32_t src = tmem + lane_base + (uint32_t)(sl * TN + colq * NC);
+                if constexpr (!kPark) {
+                    uint32_t y[NC];
 #pragma unroll
-                for (int i = 0; i < NC; ++i) {
-                    if (p == 0) yh[i] = (int32_t)y[i];
-                    else if (p < 3) yh[i] = yh[i] * 256 + (int32_t)y[i];
-                    else if (p == 3) yl[i] = (int32_t)y[i];
-                    else yl[i] = yl[i] * 256 + (int32_t)y[i];
-                }
-            }
-            if (!live) continue;
+                    for (int h = 0; h < NC / 8; ++h) tmem_ld8(src + 8 * h, y + 8 * h);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sempty[sl]);
 #pragma unroll
-            for (int i0 = 0; i0 < NC; i0 += 8) {
-                double v[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] = i64_ldexp_exact((long long)yh[i0 + i] * 16777216LL + yl[i0 + i], eadj);
-                const int64_t n0 = (int64_t)tt * kTcN + colq * NC + i0;
-                if (a.f32) {
-                    float* out = reinterpret_cast<float*>(a.beams) + ((size_t)b * a.n_dirs + slot) * a.N + n0;
-                    if (n0 + 8 <= a.L) {
-#pragma unroll
-                        for (int i = 0; i < 8; i += 4)
-                            *reinterpret_cast<float4*>(out + i) =
-                                make_float4((float)v[i], (float)v[i + 1], (float)v[i + 2], (float)v[i + 3]);
-                    } else {
-                        for (int i = 0; i < 8; ++i)
-                            if (n0 + i < a.L) out[i] = (float)v[i];
+                    for (int i = 0; i < NC; ++i) {
+                        if (p == 0) yh[i] = (int32_t)y[i];
+                        else if (p < 3) yh[i] = yh[i] * 256 + (int32_t)y[i];
+                        else if (p == 3) yl[i] = (int32_t)y[i];
+                        else yl[i] = yl[i] * 256 + (int32_t)y[i];
                     }
                 } else {
-                    double* out = reinterpret_cast<double*>(a.beams) + ((size_t)b * a.n_dirs + slot) * a.N + n0;
-                    if (n0 + 8 <= a.L) {
+                    uint32_t y[16];
 #pragma unroll
-                        for (int i = 0; i < 8; i += 4) st_global_v4(out + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                    for (int h = 0; h < 2; ++h) {
+                        tmem_ld16(src + 16 * h, y);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            yl[16 * h + i] = (p == 0 || p == 3) ? (int32_t)y[i] : yl[16 * h + i] * 256 + (int32_t)y[i];
+                    }
+                    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sempty[sl]);
+                    if (p == 2) {
+                        tmem_st16(scratch, yl);
+                        tmem_st16(scratch + 16, yl + 16);
+                        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                    }
+                }
+            }
+            // (kPark: the scratch tcgen05.ld below is warp-collective, so every
+            // lane runs the loop and only live directions store)
+            if (!kPark && !live) continue;
+#pragma unroll
+            for (int h = 0; h < NC / 16 + (NC % 16 ? 1 : 0); ++h) {
+                int32_t hi[16];
+                if constexpr (!kPark) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) hi[i] = yh[(16 * h + i) < NC ? 16 * h + i : 0];
+                } else {
+                    uint32_t u[16];
+                    tmem_ld16(scratch + 16 * h, u);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) hi[i] = (int32_t)u[i];
+                }
+#pragma unroll
+                for (int i0 = 0; i0 < 16; i0 += 8) {
+                    if (16 * h + i0 >= NC) break;
+                    double v[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        v[i] = i64_ldexp_exact((long long)hi[i0 + i] * 16777216LL + yl[16 * h + i0 + i], eadj);
+                    const int64_t n0 = (int64_t)tt * TN + colq * NC + 16 * h + i0;
+                    if (!live) continue;
+#ifdef SNB_TC_NOSTORE
+                    if (n0 >= 0) continue;
+#endif
+                    if (a.f32) {
+                        float* out = reinterpret_cast<float*>(a.beams) + ((size_t)b * a.n_dirs + slot) * a.N + n0;
+                        if (n0 + 8 <= a.L) {
+#pragma unroll
+                            for (int i = 0; i < 8; i += 4)
+                                *reinterpret_cast<float4*>(out + i) =
+                                    make_float4((float)v[i], (float)v[i + 1], (float)v[i + 2], (float)v[i + 3]);
+                        } else {
+                            for (int i = 0; i < 8; ++i)
+                                if (n0 + i < a.L) out[i] = (float)v[i];
+                        }
                     } else {
-                        for (int i = 0; i < 8; ++i)
-                            if (n0 + i < a.L) out[i] = v[i];
+                        double* out = reinterpret_cast<double*>(a.beams) + ((size_t)b * a.n_dirs + slot) * a.N + n0;
+                        if (n0 + 8 <= a.L) {
+#pragma unroll
+                            for (int i = 0; i < 8; i += 4) st_global_v4(out + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        } else {
+                            for (int i = 0; i < 8; ++i)
+                                if (n0 + i < a.L) out[i] = v[i];
+                        }
                     }
                 }
             }
@@ -430,8 +497,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
     }
 }
 
-size_t beamform_tc_smem_bytes(int rmax, int pad) {
-    const size_t need = (size_t)rmax * kABytes + kWin * (size_t)12 * (kTcN + pad) * 16 + 8 * (2 * kWin + 2 * kSlots) + 16;
+size_t beamform_tc_smem_bytes(int rmax, int pad, int tn) {
+    const size_t need = (size_t)rmax * kABytes + kWin * (size_t)12 * (tn + pad) * 16 + 8 * (2 * kWin + 2 * 8) + 16;
     // >= 115 KB so at most one CTA (and one 512-column TMEM allocation) per SM
     return need > 118 * 1024 ? need : 118 * 1024;
 }
@@ -443,13 +510,18 @@ void launch_digits(const DigitArgs& a, int batch, cudaStream_t s) {
 }
 
 void launch_beamform_tc(const TcArgs& a, const TcSched& sched, int grid, cudaStream_t s) {
-    const size_t smem = beamform_tc_smem_bytes(a.rmax, a.pad);
-    const cudaError_t e = cudaFuncSetAttribute((const void*)k_beamform_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = beamform_tc_smem_bytes(a.rmax, a.pad, a.n);
+    const void* fn = a.n == 128 ? (const void*)k_beamform_tc<128>
+                   : a.n == 96  ? (const void*)k_beamform_tc<96>
+                                : (const void*)k_beamform_tc<64>;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         fprintf(stderr, "k_beamform_tc: %zu bytes of shared memory: %s\n", smem, cudaGetErrorString(e));
         return;
     }
-    k_beamform_tc<<<grid, kTcThreads, smem, s>>>(a, sched);
+    if (a.n == 128) k_beamform_tc<128><<<grid, kTcThreads, smem, s>>>(a, sched);
+    else if (a.n == 96) k_beamform_tc<96><<<grid, kTcThreads, smem, s>>>(a, sched);
+    else k_beamform_tc<64><<<grid, kTcThreads, smem, s>>>(a, sched);
     const cudaError_t le = cudaPeekAtLastError();
     if (le != cudaSuccess) fprintf(stderr, "k_beamform_tc launch: %s\n", cudaGetErrorString(le));
 }

@@ -160,7 +160,7 @@ uint32_t crc_init_term(const uint32_t* shift, uint64_t n);
 
 // ---- tensor-core delay-and-sum (beamform_tc.cu) ---------------------------
 constexpr int kTcM = 128;      // directions per cluster (MMA M)
-constexpr int kTcN = 64;       // time samples per tile (MMA N); TMEM ring of 8 x 64 columns
+constexpr int kTcN = 64;       // narrow tile (MMA N, TMEM ring of 8 x 64); 128 where shared memory allows
 constexpr int kTcSlices = 6;   // balanced base-256 digits of the 46-bit fixed-point samples
 constexpr int kTcRMax = 40;    // max shift values per cluster (A resident in smem: 4 KB each)
 struct DigitArgs {
@@ -182,12 +182,13 @@ struct TcArgs {
     void* beams;                       // [B][n_dirs][N] slot order, f64 or f32
     int64_t L, N, n_dirs;
     int rows, pad, clusters, ntiles, batch, f32, rmax;
+    int n;                             // tile width (MMA N): 64 or 128
 };
 constexpr int kTcMaxGrid = 512;
 struct TcSched { int start[kTcMaxGrid + 1]; }; // CTA k processes tiles [start[k], start[k+1])
 void launch_digits(const DigitArgs& a, int batch, cudaStream_t s);
 void launch_beamform_tc(const TcArgs& a, const TcSched& sched, int grid, cudaStream_t s);
-size_t beamform_tc_smem_bytes(int rmax, int pad);
+size_t beamform_tc_smem_bytes(int rmax, int pad, int tn);
 
 size_t demod_smem_bytes(int octets, int words);
 size_t fft_smem_bytes(int n, int real_bytes);

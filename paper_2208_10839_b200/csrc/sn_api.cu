@@ -181,7 +181,7 @@ struct sn_workspace {
     int32_t* h_crc_ok = nullptr;
     // tensor-core beamformer (beamform_tc.cu)
     bool tc = false;
-    int tc_clusters = 0, tc_pad = 0, tc_rows = 0, tc_ntiles = 0, tc_grid = 0;
+    int tc_clusters = 0, tc_pad = 0, tc_rows = 0, tc_ntiles = 0, tc_grid = 0, tc_n = kTcN;
     std::vector<int32_t> tc_R;
     int8_t* d_planes = nullptr;
     uint2* d_dwords = nullptr;
@@ -514,8 +514,16 @@ struct sn_workspace {
         tc_clusters = (int)tc_R.size();
         tc_rmax = *std::max_element(tc_R.begin(), tc_R.end());
         tc_pad = (tc_rmax + 6) & ~7; // >= rmax - 1, multiple of 8
-        tc_ntiles = (int)((s.mf_len + kTcN - 1) / kTcN);
-        tc_rows = tc_pad + tc_ntiles * kTcN;
+        // wide tiles (N = 128: 3 TMEM slots, ~1.4x the int8 MMA rate per
+        // instruction) when the resident A_r and three B windows fit in
+        // shared memory; SNB_TC_N=64 forces the narrow tiles
+        const char* ev = getenv("SNB_TC_N");
+        const int want = ev ? atoi(ev) : 96;
+        tc_n = kTcN;
+        for (int n : {128, 96})
+            if (want >= n && tc_n == kTcN && beamform_tc_smem_bytes(tc_rmax, tc_pad, n) <= 200 * 1024) tc_n = n;
+        tc_ntiles = (int)((s.mf_len + tc_n - 1) / tc_n);
+        tc_rows = tc_pad + tc_ntiles * tc_n;
     }
 
     void init_tensor_core_beamformer(int sms) {
@@ -603,6 +611,7 @@ struct sn_workspace {
             ta.ntiles = tc_ntiles;
             ta.batch = (int)count;
             ta.f32 = f32 ? 1 : 0;
+            ta.n = tc_n;
             launch_beamform_tc(ta, tc_schedule((int)count), tc_grid, s);
         } else {
         BeamArgs ba{};
@@ -1185,7 +1194,7 @@ sn_status sn_workspace_beamformer_info(const sn_workspace* ws, sn_beamformer_inf
         info->ntiles = ws->tc_ntiles;
         info->slices = kTcSlices;
         info->m = kTcM;
-        info->n = kTcN;
+        info->n = ws->tc_n;
         info->k = 32;
     });
 }

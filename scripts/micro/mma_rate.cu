@@ -65,4 +65,5 @@ template <int N, int ROT, bool TS = false> void run(int sms) {
 int main() {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     run<32,2>(sms); run<32,2,true>(sms); run<64,2>(sms); run<64,2,true>(sms); run<128,2>(sms); run<128,2,true>(sms);
+    run<64,1>(sms); run<128,1>(sms); run<64,6>(sms); run<128,3>(sms);
 }
