@@ -145,10 +145,11 @@ __device__ __forceinline__ int bfp_exponent(unsigned long long amax_bits) {
 }
 
 
-// TMEM ring of accumulator slots of TN columns: 8 x 64, or 3 x 128 with the
-// last 128 columns the epilogue's scratch (Y_hi parked between planes)
-template <int TN> constexpr int slots_for() { return TN == 64 ? 8 : TN == 96 ? 5 : 3; }
-constexpr int kWin = 3;                       // B window buffers (loads run kWin - 1 tiles ahead)
+// TMEM ring of accumulator slots of TN columns: 8 x 64, 5 x 96 or 4 x 128
+template <int TN> constexpr int slots_for() { return TN == 64 ? 8 : TN == 96 ? 5 : 4; }
+// B window buffers (loads run kWin - 1 tiles ahead); 2 for N = 128, whose
+// epilogue parks Y_hi in shared memory
+constexpr int win_for(int tn) { return tn == 128 ? 2 : 3; }
 constexpr int kEpiWarps = 16;                  // epilogue warps; warp 8 produces and issues
 constexpr int kTcThreads = 32 * (kEpiWarps + 1);
 constexpr int kTmemCols = 512;
@@ -260,6 +261,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 template <int TN>
 __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const __grid_constant__ TcSched sched) {
     constexpr int kSlots = slots_for<TN>();
+    constexpr int kWin = win_for(TN);
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wrows = TN + a.pad;                       // window rows per (digit, half)
@@ -272,6 +274,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
     uint64_t* sfull = bars + 2 * kWin;  // [kSlots]
     uint64_t* sempty = sfull + kSlots;  // [kSlots]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + kSlots);
+    // N = 128: Y_hi of every epilogue thread, [8][kEpiWarps * 32] x 16 B
+    uint4* park = reinterpret_cast<uint4*>(bars + 2 * kWin + 2 * 8 + 2);
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
                      "n"(kTmemCols)
@@ -383,10 +387,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
         const int quarter = warp & 3, colq = warp >> 2;
         const int d = quarter * 32 + lane;
         constexpr int NC = TN / 4; // columns per thread
-        constexpr bool kPark = TN == 128; // Y_hi parked in TMEM scratch columns (register budget)
+        constexpr bool kPark = TN == 128; // Y_hi parked in shared memory (register budget)
         static_assert(NC % 8 == 0 && (!kPark || NC == 32), "epilogue column chunks");
         const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-        const uint32_t scratch = tmem + lane_base + (uint32_t)(kSlots * TN + colq * NC); // kPark only
         for (int g = 0; g < ntile; ++g) {
             const int t = t_beg + g;
             const int c = t / per_cb, rem = t - c * per_cb;
@@ -431,15 +434,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&sempty[sl]);
                     if (p == 2) {
-                        tmem_st16(scratch, yl);
-                        tmem_st16(scratch + 16, yl + 16);
-                        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            park[k * (kEpiWarps * 32) + tid] =
+                                make_uint4(yl[4 * k], yl[4 * k + 1], yl[4 * k + 2], yl[4 * k + 3]);
                     }
                 }
             }
-            // (kPark: the scratch tcgen05.ld below is warp-collective, so every
-            // lane runs the loop and only live directions store)
-            if (!kPark && !live) continue;
+            if (!live) continue;
 #pragma unroll
             for (int h = 0; h < NC / 16 + (NC % 16 ? 1 : 0); ++h) {
                 int32_t hi[16];
@@ -447,11 +449,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
 #pragma unroll
                     for (int i = 0; i < 16; ++i) hi[i] = yh[(16 * h + i) < NC ? 16 * h + i : 0];
                 } else {
-                    uint32_t u[16];
-                    tmem_ld16(scratch + 16 * h, u);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) hi[i] = (int32_t)u[i];
+                    for (int k = 0; k < 4; ++k) {
+                        const uint4 u = park[(4 * h + k) * (kEpiWarps * 32) + tid];
+                        hi[4 * k] = (int32_t)u.x;
+                        hi[4 * k + 1] = (int32_t)u.y;
+                        hi[4 * k + 2] = (int32_t)u.z;
+                        hi[4 * k + 3] = (int32_t)u.w;
+                    }
                 }
 #pragma unroll
                 for (int i0 = 0; i0 < 16; i0 += 8) {
@@ -461,7 +466,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
                     for (int i = 0; i < 8; ++i)
                         v[i] = i64_ldexp_exact((long long)hi[i0 + i] * 16777216LL + yl[16 * h + i0 + i], eadj);
                     const int64_t n0 = (int64_t)tt * TN + colq * NC + 16 * h + i0;
-                    if (!live) continue;
 #ifdef SNB_TC_NOSTORE
                     if (n0 >= 0) continue;
 #endif
@@ -498,7 +502,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
 }
 
 size_t beamform_tc_smem_bytes(int rmax, int pad, int tn) {
-    const size_t need = (size_t)rmax * kABytes + kWin * (size_t)12 * (tn + pad) * 16 + 8 * (2 * kWin + 2 * 8) + 16;
+    const size_t need = (size_t)rmax * kABytes + win_for(tn) * (size_t)12 * (tn + pad) * 16 +
+                        8 * (2 * win_for(tn) + 2 * 8 + 2) + (tn == 128 ? (size_t)8 * kEpiWarps * 32 * 16 : 0);
     // >= 115 KB so at most one CTA (and one 512-column TMEM allocation) per SM
     return need > 118 * 1024 ? need : 118 * 1024;
 }

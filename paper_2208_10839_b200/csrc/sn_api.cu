@@ -521,7 +521,7 @@ struct sn_workspace {
         const int want = ev ? atoi(ev) : 96;
         tc_n = kTcN;
         for (int n : {128, 96})
-            if (want >= n && tc_n == kTcN && beamform_tc_smem_bytes(tc_rmax, tc_pad, n) <= 200 * 1024) tc_n = n;
+            if (want >= n && tc_n == kTcN && beamform_tc_smem_bytes(tc_rmax, tc_pad, n) <= 220 * 1024) tc_n = n;
         tc_ntiles = (int)((s.mf_len + tc_n - 1) / tc_n);
         tc_rows = tc_pad + tc_ntiles * tc_n;
     }
