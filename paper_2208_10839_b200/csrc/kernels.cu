@@ -29,6 +29,7 @@ namespace snb {
 // over octets t = 0 .. 4*floor(T/4)-1 (lane t mod 4), (a0+a1)+(a2+a3), then
 // the remaining octets in order; adds only, every add rounded (DADD).
 // ---------------------------------------------------------------------------
+constexpr int kDemodOctets = 33; // the default 255-tap demodulator: 33 octets per output
 __global__ void __launch_bounds__(kThreads) k_demod(DemodArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* lut = reinterpret_cast<double*>(smem);
@@ -87,8 +88,34 @@ __global__ void __launch_bounds__(kThreads) k_demod(DemodArgs a) {
             double v = 0.0;
             if (m >= a.m_lo && m < a.m_hi) {
                 const int64_t s = (int64_t)a.decim * m - a.center;
-                const uint8_t* rb =
-                    reinterpret_cast<const uint8_t*>(rows + c * a.words) + ((s - F0) >> 3);
+                const int off = (int)((s - F0) >> 3); // first octet (byte) of the window in the row
+                if (T == kDemodOctets) {
+                    // the window's 33 bytes from 10 aligned words, re-aligned by
+                    // funnel shifts (10 shared loads instead of 33 byte loads)
+                    const uint32_t* rw = rows + c * a.words + (off >> 2);
+                    const int sh = 8 * (off & 3);
+                    uint32_t w[10];
+#pragma unroll
+                    for (int i = 0; i < 10; ++i) w[i] = rw[i];
+                    uint32_t aw[9];
+#pragma unroll
+                    for (int i = 0; i < 9; ++i) aw[i] = __funnelshift_r(w[i], w[i + 1], sh);
+                    auto lv = [&](int t) { return lut[t * 256 + ((aw[t >> 2] >> (8 * (t & 3))) & 255u)]; };
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+                    for (int t = 0; t + 4 <= kDemodOctets; t += 4) {
+                        a0 = __dadd_rn(a0, lv(t + 0));
+                        a1 = __dadd_rn(a1, lv(t + 1));
+                        a2 = __dadd_rn(a2, lv(t + 2));
+                        a3 = __dadd_rn(a3, lv(t + 3));
+                    }
+                    double acc = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+#pragma unroll
+                    for (int t = kDemodOctets & ~3; t < kDemodOctets; ++t) acc = __dadd_rn(acc, lv(t));
+                    out_b[(size_t)c * a.demod_len + m] = acc;
+                    continue;
+                }
+                const uint8_t* rb = reinterpret_cast<const uint8_t*>(rows + c * a.words) + off;
                 double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
                 int t = 0;
                 for (; t + 4 <= T; t += 4) {
