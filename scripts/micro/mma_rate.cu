@@ -9,12 +9,12 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
            ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46);
 }
-template <int N, int ROT, bool TS = false>
+template <int N, int ROT, bool TS = false, bool VAR = false>
 __global__ void k(int iters, int* out) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t slot;
     __shared__ __align__(8) uint64_t bar;
-    for (int i = threadIdx.x; i < 128 * 32 + N * 32; i += blockDim.x) smem[i] = (uint8_t)(i * 7);
+    for (int i = threadIdx.x; i < 20 * 128 * 32 + (N + 32) * 32; i += blockDim.x) smem[i] = (uint8_t)(i * 7);
     if (threadIdx.x < 32) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(&slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -35,6 +35,18 @@ __global__ void k(int iters, int* out) {
                          "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)((it % ROT) * N)),
                          "r"(tmem + 384u), "l"(bd), "r"(idesc), "r"(1));
           }
+        } else if (VAR) {
+          // as k_beamform_tc: 20 resident A_r (4 KB apart), B window shifted by one 16-byte row per r
+          const uint64_t bd0 = sdesc(su32(smem + 20 * 128 * 32 + 19 * 16), (N + 32) * 16, 128);
+          for (int it = 0; it < iters; it += 20) {
+            uint64_t a_ = sdesc(su32(smem), 128 * 16, 128), b_ = bd0;
+            for (int r = 0; r < 20; ++r) {
+              asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                           "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(((it / 20) % 2) * N)),
+                           "l"(a_), "l"(b_), "r"(idesc), "r"(r));
+              a_ += 256; b_ -= 1;
+            }
+          }
         } else
         for (int it = 0; it < iters; ++it) {
             asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -49,21 +61,22 @@ __global__ void k(int iters, int* out) {
     if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
     if (threadIdx.x == 0 && out) out[blockIdx.x] = 1;
 }
-template <int N, int ROT, bool TS = false> void run(int sms) {
+template <int N, int ROT, bool TS = false, bool VAR = false> void run(int sms) {
     const int iters = 20000;
-    cudaFuncSetAttribute(k<N, ROT, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
-    k<N, ROT, TS><<<sms, 128, 150 * 1024>>>(100, nullptr);
+    cudaFuncSetAttribute(k<N, ROT, TS, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
+    k<N, ROT, TS, VAR><<<sms, 128, 150 * 1024>>>(100, nullptr);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     cudaEventRecord(a);
-    k<N, ROT, TS><<<sms, 128, 150 * 1024>>>(iters, nullptr);
+    k<N, ROT, TS, VAR><<<sms, 128, 150 * 1024>>>(iters, nullptr);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
     const double macs = (double)sms * iters * 128.0 * N * 32;
-    printf("TS=%d ROT=%d ", (int)TS, ROT); printf("N=%3d: %.3f ms, %.2f TOPS (int8, 2 ops/MAC), %.1f clk/MMA at 1.965 GHz, err=%s\n", N, ms, 2 * macs / ms / 1e9,
+    printf("TS=%d ROT=%d VAR=%d ", (int)TS, ROT, (int)VAR); printf("N=%3d: %.3f ms, %.2f TOPS (int8, 2 ops/MAC), %.1f clk/MMA at 1.965 GHz, err=%s\n", N, ms, 2 * macs / ms / 1e9,
            ms * 1e-3 * 1.965e9 / iters, cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     run<32,2>(sms); run<32,2,true>(sms); run<64,2>(sms); run<64,2,true>(sms); run<128,2>(sms); run<128,2,true>(sms);
     run<64,1>(sms); run<128,1>(sms); run<64,6>(sms); run<128,3>(sms);
+    run<64,2,false,true>(sms); run<96,2,false,true>(sms); run<128,2,false,true>(sms); run<96,2>(sms);
 }
