@@ -393,6 +393,27 @@ def test_tensor_core_beamformer_vs_tiled_and_reference(gpu, po, ref, name, monke
     assert ws_c.process(m).energies.tobytes() == e_c.tobytes()  # deterministic (integer MMA)
 
 
+@pytest.mark.parametrize("tile_n", [64, 96, 128])
+def test_tensor_core_tile_widths(gpu, po, ref, tile_n, monkeypatch):
+    # the three MMA tile widths (N = 64: 8 TMEM slots; 96: 5; 128: 4 slots with
+    # Y_hi parked in shared memory) give identical energyscapes (exact integer
+    # sums) within one ulp of the reference; a 1-capture and a 3-capture batch
+    sn = gpu
+    cfg = cfg_for(sn, "box1850")
+    monkeypatch.setenv("SNB_BEAMFORMER", "tc")
+    monkeypatch.setenv("SNB_TC_N", str(tile_n))
+    ws = sn.Workspace(cfg, device=0, max_batch=3)
+    assert ws.beamformer_info()["n"] == tile_n
+    ms = [capture(sn, cfg, [(1.0 + 0.3 * i, 0.2 - 0.1 * i, 0.1, 0.7)], 0.01, 21 + i, seq=i) for i in range(3)]
+    e = np.stack([im.energies for im in ws.process_batch(ms)])
+    r = ref.workspace(to_oracle(po, cfg))
+    for i in range(3):
+        check_f64(e[i], r.process(ms[i].packed))
+    monkeypatch.setenv("SNB_TC_N", "64")
+    base = sn.Workspace(cfg, device=0, max_batch=3)
+    assert np.array_equal(np.stack([im.energies for im in base.process_batch(ms)]), e)
+
+
 def test_tensor_core_beamformer_scale_invariance(gpu):
     # block floating point: the quantisation scale follows max|filt| of each
     # capture, so silence and a strong echo in one batch do not interact
