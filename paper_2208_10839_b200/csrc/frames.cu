@@ -84,69 +84,103 @@ __global__ void __launch_bounds__(kCrcThreads) k_crc_partial(const uint8_t* base
 // Image-frame encoder: frame f (stride fstride) from the f32 energyscape
 // energies[f][n_dirs * bins] and the header template; CRC of bytes
 // [0, frame_len - 4) accumulated into acc[f].
+// One warp per 4 KB segment of the frame: the words are produced and stored
+// lane-interleaved (coalesced loads of the energies, coalesced stores) and
+// staged in shared memory; lane l then CRCs its contiguous 128-byte chunk,
+// moves it to the segment end with the constant map A_{128 (31 - l)}
+// (CrcTables::lane), the warp XOR-reduces, and lane 0 moves the segment's CRC
+// to the frame end. Frame words: template (header fields patched per capture)
+// up to byte E - 2; the word at E - 2 joins the template's last two bytes and
+// the low half of energy 0; above, word = hi16(en[q]) | lo16(en[q + 1]) << 16;
+// the CRC covers a final 2-byte tail (hi16 of the last energy).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kCrcThreads) k_encode_image_frames(ImageFrameArgs a, CrcTables ct) {
+constexpr int kEncWarps = 8, kSegWords = 1024;
+
+__global__ void __launch_bounds__(32 * kEncWarps) k_encode_image_frames(ImageFrameArgs a, CrcTables ct) {
     __shared__ uint32_t s_tab[1024];
+    __shared__ uint32_t s_lane[1024];
+    __shared__ uint32_t s_w[kEncWarps][kSegWords + 32];
     load_crc_tables(ct, s_tab);
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_lane[i] = ct.lane[i];
     __syncthreads();
-    const int f = blockIdx.y;
-    const uint64_t F = a.frame_len, ncrc = F - 4;
-    const uint64_t c0 = ((uint64_t)blockIdx.x * kCrcThreads + threadIdx.x) * kCrcChunk;
-    if (c0 >= ncrc) return;
-    const uint64_t c1 = c0 + kCrcChunk < ncrc ? c0 + kCrcChunk : ncrc;
+    const int f = blockIdx.y, warp = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const uint64_t ncrc = a.frame_len - 4; // = E + 4 cells, E % 4 == 2
+    const uint64_t nw = ncrc / 4;          // full words; then the 2-byte tail at byte 4 nw
+    const uint64_t w0 = ((uint64_t)blockIdx.x * kEncWarps + warp) * kSegWords;
+    if (w0 > nw) return;
     uint8_t* out = a.frames + (size_t)f * a.frame_stride;
+    uint32_t* ow = reinterpret_cast<uint32_t*>(out);
     const uint32_t* en = reinterpret_cast<const uint32_t*>(a.energies + (size_t)f * a.cells);
     const uint8_t* tpl = a.tpl;
+    const uint32_t* tplw = reinterpret_cast<const uint32_t*>(tpl);
     const FrameIds id = a.ids[f];
-    const uint64_t E = a.tpl_len; // first energy byte (E % 4 == 2)
-    auto byte_at = [&](uint64_t b) -> uint32_t {
-        if (b < E) {
-            // header fields patched per capture (packet: serial 8, ts 12, seq 20;
-            // AIMG: serial 42, ts 46)
-            if (b >= 8 && b < 12) return (id.serial >> (8 * (b - 8))) & 0xFF;
-            if (b >= 12 && b < 20) return (uint32_t)(id.ts >> (8 * (b - 12))) & 0xFF;
-            if (b >= 20 && b < 28) return (uint32_t)(id.seq >> (8 * (b - 20))) & 0xFF;
-            if (b >= 42 && b < 46) return (id.serial >> (8 * (b - 42))) & 0xFF;
-            if (b >= 46 && b < 54) return (uint32_t)(id.ts >> (8 * (b - 46))) & 0xFF;
-            return tpl[b];
-        }
-        const uint64_t e = b - E;
-        return (__ldg(en + e / 4) >> (8 * (e & 3))) & 0xFF;
+    const uint64_t E = a.tpl_len;
+    auto tpl_byte = [&](uint64_t b) -> uint32_t {
+        // header fields patched per capture (packet: serial 8, ts 12, seq 20;
+        // AIMG: serial 42, ts 46)
+        if (b >= 8 && b < 12) return (id.serial >> (8 * (b - 8))) & 0xFF;
+        if (b >= 12 && b < 20) return (uint32_t)(id.ts >> (8 * (b - 12))) & 0xFF;
+        if (b >= 20 && b < 28) return (uint32_t)(id.seq >> (8 * (b - 20))) & 0xFF;
+        if (b >= 42 && b < 46) return (id.serial >> (8 * (b - 42))) & 0xFF;
+        if (b >= 46 && b < 54) return (uint32_t)(id.ts >> (8 * (b - 46))) & 0xFF;
+        return tpl[b];
     };
-    uint32_t c = 0;
-    uint64_t b = c0;
-    uint32_t* ow = reinterpret_cast<uint32_t*>(out);
-    // bytes below the first full energy word, and the partial last word: byte path
-    const uint64_t fast0 = E + 2;            // 4-aligned, first word made of two energy halves
-    const uint64_t fast1 = ncrc & ~uint64_t(3); // words below this are complete
-    while (b < c1 && (b < fast0 || b >= fast1 || (b & 3))) {
-        const uint32_t v = byte_at(b);
-        if ((b & 3) == 0 && b + 4 <= c1 && b + 4 <= ncrc && b < fast0) {
-            // whole header word
-            const uint32_t word = v | (byte_at(b + 1) << 8) | (byte_at(b + 2) << 16) | (byte_at(b + 3) << 24);
-            ow[b / 4] = word;
-            c = crc_word(s_tab, c, word);
-            b += 4;
-            continue;
+    auto word_at = [&](uint64_t w) -> uint32_t {
+        const uint64_t b = 4 * w;
+        if (b + 4 <= E - 2) {
+            if (b >= 56) return __ldg(tplw + w);
+            return tpl_byte(b) | (tpl_byte(b + 1) << 8) | (tpl_byte(b + 2) << 16) | (tpl_byte(b + 3) << 24);
         }
-        out[b] = (uint8_t)v;
-        c = crc_byte(s_tab, c, v);
-        ++b;
-    }
-    // fast path: word w at byte 4w >= E + 2: hi16(en[q]) | lo16(en[q + 1]) << 16
-    for (; b + 4 <= c1 && b + 4 <= fast1; b += 4) {
+        if (b == E - 2) return (uint32_t)tpl[E - 2] | ((uint32_t)tpl[E - 1] << 8) | (__ldg(en) << 16);
         const uint64_t q = (b - E - 2) / 4;
-        const uint32_t word = __funnelshift_r(__ldg(en + q), __ldg(en + q + 1), 16);
-        ow[b / 4] = word;
-        c = crc_word(s_tab, c, word);
+        return __funnelshift_r(__ldg(en + q), __ldg(en + q + 1), 16);
+    };
+    const uint32_t tail = __ldg(en + a.cells - 1) >> 16;
+    uint32_t* sw = s_w[warp];
+#pragma unroll 4
+    for (int i = 0; i < 32; ++i) {
+        const uint64_t w = w0 + 32 * i + l;
+        if (w < nw) {
+            const uint32_t v = word_at(w);
+            ow[w] = v;
+            sw[33 * i + l] = v;
+        } else if (w == nw) {
+            reinterpret_cast<uint16_t*>(out + 4 * nw)[0] = (uint16_t)tail;
+        }
     }
-    for (; b < c1; ++b) {
-        const uint32_t v = byte_at(b);
-        out[b] = (uint8_t)v;
-        c = crc_byte(s_tab, c, v);
+    __syncwarp();
+    uint32_t c = 0;
+    const uint64_t cw0 = w0 + 32 * l; // lane chunk: words [cw0, cw0 + 32)
+    for (int i = 0; i < 32; ++i) {
+        const uint64_t w = cw0 + i;
+        if (w < nw) {
+            c = crc_word(s_tab, c, sw[33 * l + i]);
+        } else {
+            if (w == nw) {
+                c = crc_byte(s_tab, c, tail & 0xFF);
+                c = crc_byte(s_tab, c, tail >> 8);
+            }
+            break;
+        }
     }
-    c = crc_shift(ct.shift, c, ncrc - c1);
-    if (c) atomicXor(a.acc + f, c);
+    const bool full = w0 + kSegWords <= nw;
+    if (full) {
+        // A_{128 (31 - l)}: to the segment end
+        const uint32_t* col = s_lane + 32 * l;
+        uint32_t r = 0;
+#pragma unroll
+        for (int b = 0; b < 32; ++b) r ^= (0u - ((c >> b) & 1u)) & col[b];
+        c = r;
+    } else {
+        const uint64_t end = cw0 + 32 <= nw ? 4 * (cw0 + 32) : ncrc;
+        c = cw0 <= nw ? crc_shift(ct.shift, c, ncrc - end) : 0u;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
+    if (l == 0) {
+        if (full) c = crc_shift(ct.shift, c, ncrc - 4 * (w0 + kSegWords));
+        if (c) atomicXor(a.acc + f, c);
+    }
 }
 
 // crc[f] = acc[f] ^ k_n (k_n = A_n(~0) ^ ~0 from the host); optionally stored
@@ -178,9 +212,9 @@ void launch_crc_partial(const uint8_t* base, uint64_t stride, uint64_t n, uint64
 }
 
 void launch_encode_image_frames(const ImageFrameArgs& a, uint64_t count, const CrcTables& ct, cudaStream_t s) {
-    const uint64_t chunks = (a.frame_len - 4 + kCrcChunk - 1) / kCrcChunk;
-    const unsigned gx = (unsigned)((chunks + kCrcThreads - 1) / kCrcThreads);
-    k_encode_image_frames<<<dim3(gx, (unsigned)count), kCrcThreads, 0, s>>>(a, ct);
+    const uint64_t segs = ((a.frame_len - 4) / 4 + 1 + kSegWords - 1) / kSegWords; // words + the tail
+    const unsigned gx = (unsigned)((segs + kEncWarps - 1) / kEncWarps);
+    k_encode_image_frames<<<dim3(gx, (unsigned)count), 32 * kEncWarps, 0, s>>>(a, ct);
 }
 
 void launch_crc_finalize(uint32_t* acc, uint32_t k_n, uint64_t count, uint8_t* out, uint64_t stride, uint64_t n,
@@ -236,6 +270,18 @@ void crc_tables_host(uint32_t* slice /* 1024 */, uint32_t* shift /* kCrcShiftMat
         }
         for (int b = 0; b < 32; ++b) m[b] = sq[b];
     }
+}
+
+uint32_t crc_advance_host(const uint32_t* shift, uint32_t v, uint64_t n) {
+    for (int k = 0; n != 0 && v != 0; ++k, n >>= 1) {
+        if (n & 1) {
+            uint32_t r = 0;
+            for (int b = 0; b < 32; ++b)
+                if (v >> b & 1) r ^= shift[32 * k + b];
+            v = r;
+        }
+    }
+    return v;
 }
 
 uint32_t crc_init_term(const uint32_t* shift, uint64_t n) {

@@ -117,6 +117,7 @@ constexpr int kCrcShiftMats = 48;   // A_{2^k}, k < 48: messages up to 2^48 byte
 struct CrcTables {
     const uint32_t* slice;          // [4][256] slicing-by-4 tables
     const uint32_t* shift;          // [kCrcShiftMats][32] columns of A_{2^k}
+    const uint32_t* lane;           // [32][32] columns of A_{128 (31 - l)} (warp-segment encoder)
 };
 struct FrameIds {                   // per-capture header fields
     uint32_t serial;
@@ -157,6 +158,8 @@ struct SynthArgs {
 void launch_synth(const SynthArgs& a, cudaStream_t s);
 void crc_tables_host(uint32_t* slice, uint32_t* shift);
 uint32_t crc_init_term(const uint32_t* shift, uint64_t n);
+// A_n(v) on the host (shift: crc_tables_host's A_{2^k} columns)
+uint32_t crc_advance_host(const uint32_t* shift, uint32_t v, uint64_t n);
 
 // ---- tensor-core delay-and-sum (beamform_tc.cu) ---------------------------
 constexpr int kTcM = 128;      // directions per cluster (MMA M)

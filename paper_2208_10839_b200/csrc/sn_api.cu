@@ -166,6 +166,7 @@ struct sn_workspace {
     // wire-format frames (frames.cu)
     uint32_t* d_crc_slice = nullptr;
     uint32_t* d_crc_shift = nullptr;
+    uint32_t* d_crc_lane = nullptr;
     std::vector<uint32_t> h_crc_shift;
     uint8_t* d_img_tpl = nullptr;
     uint64_t img_tpl_len = 0, img_frame_len = 0, img_frame_stride = 0;
@@ -225,7 +226,7 @@ struct sn_workspace {
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
                         (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32, (void*)d_tw_small, (void*)d_tw_small32, (void*)d_planes, (void*)d_dwords, (void*)d_resid,
                         (void*)d_tc_R, (void*)d_tc_base, (void*)d_amax, (void*)d_tc_start, (void*)d_tc_size,
-                        (void*)d_crc_slice, (void*)d_crc_shift, (void*)d_img_tpl, (void*)d_frames_out,
+                        (void*)d_crc_slice, (void*)d_crc_shift, (void*)d_crc_lane, (void*)d_img_tpl, (void*)d_frames_out,
                         (void*)d_frames_in, (void*)d_ids, (void*)d_crc_acc, (void*)d_crc_ok}) {
             if (p) cudaFree(p);
         }
@@ -433,6 +434,11 @@ struct sn_workspace {
         d_crc_shift = dmalloc<uint32_t>(h_crc_shift.size(), n);
         upload(d_crc_slice, slice, stream);
         upload(d_crc_shift, h_crc_shift, stream);
+        std::vector<uint32_t> lane(1024);
+        for (int l = 0; l < 32; ++l)
+            for (int b = 0; b < 32; ++b) lane[32 * l + b] = crc_advance_host(h_crc_shift.data(), 1u << b, 128u * (31 - l));
+        d_crc_lane = dmalloc<uint32_t>(lane.size(), n);
+        upload(d_crc_lane, lane, stream);
         const auto tpl = image_template();
         img_tpl_len = tpl.size();
         img_frame_len = img_tpl_len + 4 * z.n_dirs * z.bins + 4;
@@ -452,7 +458,7 @@ struct sn_workspace {
         ck(cudaMallocHost(&h_ids, B * sizeof(FrameIds)), "cudaMallocHost");
         ck(cudaMallocHost(&h_crc_ok, B * sizeof(int32_t)), "cudaMallocHost");
     }
-    CrcTables crc_tables() const { return CrcTables{d_crc_slice, d_crc_shift}; }
+    CrcTables crc_tables() const { return CrcTables{d_crc_slice, d_crc_shift, d_crc_lane}; }
 
     // Tensor-core delay-and-sum setup (beamform_tc.cu): clusters of <= kTcM
     // consecutive slots cut greedily so that R_c (the largest per-channel
