@@ -26,8 +26,6 @@ namespace snb {
 
 namespace {
 
-constexpr int kCrcThreads = 256;
-
 __device__ __forceinline__ uint32_t crc_word(const uint32_t* __restrict__ t, uint32_t c, uint32_t w) {
     c ^= w; // little-endian: byte 0 first
     return t[768 + (c & 0xFF)] ^ t[512 + ((c >> 8) & 0xFF)] ^ t[256 + ((c >> 16) & 0xFF)] ^ t[c >> 24];
@@ -59,25 +57,67 @@ __device__ __forceinline__ void load_crc_tables(const CrcTables& ct, uint32_t* s
 // ---------------------------------------------------------------------------
 // CRC of `count` byte strings (string f at base + f * stride, n bytes each,
 // base and stride 4-byte aligned): acc[f] ^= XOR of shifted chunk CRCs.
-// Chunks of kCrcChunk bytes per thread.
+// One warp per 4 KB segment (see the encoder below): coalesced word loads
+// staged in shared memory, a 128-byte chunk per lane, lane chunks moved to
+// the segment end by the constant maps A_{128 (31 - l)}, segments to the
+// string end by A_{2^k} products; the n mod 4 trailing bytes by the byte table.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kCrcThreads) k_crc_partial(const uint8_t* base, uint64_t stride, uint64_t n,
-                                                             CrcTables ct, uint32_t* acc) {
+constexpr int kEncWarps = 8, kSegWords = 1024;
+
+__device__ __forceinline__ uint32_t lane_to_segment_end(const uint32_t* s_lane, int l, uint32_t c) {
+    const uint32_t* col = s_lane + 32 * l;
+    uint32_t r = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) r ^= (0u - ((c >> b) & 1u)) & col[b];
+    return r;
+}
+
+__global__ void __launch_bounds__(32 * kEncWarps) k_crc_partial(const uint8_t* base, uint64_t stride, uint64_t n,
+                                                                CrcTables ct, uint32_t* acc) {
     __shared__ uint32_t s_tab[1024];
+    __shared__ uint32_t s_lane[1024];
+    __shared__ uint32_t s_w[kEncWarps][kSegWords + 32];
     load_crc_tables(ct, s_tab);
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_lane[i] = ct.lane[i];
     __syncthreads();
-    const int f = blockIdx.y;
-    const uint64_t c0 = ((uint64_t)blockIdx.x * kCrcThreads + threadIdx.x) * kCrcChunk;
-    if (c0 >= n) return;
-    const uint64_t c1 = c0 + kCrcChunk < n ? c0 + kCrcChunk : n;
+    const int f = blockIdx.y, warp = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const uint64_t nw = n / 4; // full words; then n % 4 tail bytes
+    const uint64_t w0 = ((uint64_t)blockIdx.x * kEncWarps + warp) * kSegWords;
+    if (w0 > nw || (w0 == nw && (n & 3) == 0)) return;
     const uint8_t* p = base + (size_t)f * stride;
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(p + c0);
+    const uint32_t* pw = reinterpret_cast<const uint32_t*>(p);
+    uint32_t* sw = s_w[warp];
+#pragma unroll 4
+    for (int i = 0; i < 32; ++i) {
+        const uint64_t w = w0 + 32 * i + l;
+        if (w < nw) sw[33 * i + l] = __ldg(pw + w);
+    }
+    __syncwarp();
     uint32_t c = 0;
-    const uint64_t nw = (c1 - c0) / 4;
-    for (uint64_t i = 0; i < nw; ++i) c = crc_word(s_tab, c, __ldg(w + i));
-    for (uint64_t b = c0 + 4 * nw; b < c1; ++b) c = crc_byte(s_tab, c, p[b]);
-    c = crc_shift(ct.shift, c, n - c1);
-    if (c) atomicXor(acc + f, c);
+    const uint64_t cw0 = w0 + 32 * l;
+    for (int i = 0; i < 32; ++i) {
+        const uint64_t w = cw0 + i;
+        if (w < nw) {
+            c = crc_word(s_tab, c, sw[33 * l + i]);
+        } else {
+            if (w == nw)
+                for (uint64_t bb = 4 * nw; bb < n; ++bb) c = crc_byte(s_tab, c, p[bb]);
+            break;
+        }
+    }
+    const bool full = w0 + kSegWords <= nw;
+    if (full) {
+        c = lane_to_segment_end(s_lane, l, c);
+    } else {
+        const uint64_t end = cw0 + 32 <= nw ? 4 * (cw0 + 32) : n;
+        c = cw0 <= nw ? crc_shift(ct.shift, c, n - end) : 0u;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
+    if (l == 0) {
+        if (full) c = crc_shift(ct.shift, c, n - 4 * (w0 + kSegWords));
+        if (c) atomicXor(acc + f, c);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -94,8 +134,6 @@ __global__ void __launch_bounds__(kCrcThreads) k_crc_partial(const uint8_t* base
 // the low half of energy 0; above, word = hi16(en[q]) | lo16(en[q + 1]) << 16;
 // the CRC covers a final 2-byte tail (hi16 of the last energy).
 // ---------------------------------------------------------------------------
-constexpr int kEncWarps = 8, kSegWords = 1024;
-
 __global__ void __launch_bounds__(32 * kEncWarps) k_encode_image_frames(ImageFrameArgs a, CrcTables ct) {
     __shared__ uint32_t s_tab[1024];
     __shared__ uint32_t s_lane[1024];
@@ -165,12 +203,7 @@ __global__ void __launch_bounds__(32 * kEncWarps) k_encode_image_frames(ImageFra
     }
     const bool full = w0 + kSegWords <= nw;
     if (full) {
-        // A_{128 (31 - l)}: to the segment end
-        const uint32_t* col = s_lane + 32 * l;
-        uint32_t r = 0;
-#pragma unroll
-        for (int b = 0; b < 32; ++b) r ^= (0u - ((c >> b) & 1u)) & col[b];
-        c = r;
+        c = lane_to_segment_end(s_lane, l, c);
     } else {
         const uint64_t end = cw0 + 32 <= nw ? 4 * (cw0 + 32) : ncrc;
         c = cw0 <= nw ? crc_shift(ct.shift, c, ncrc - end) : 0u;
@@ -206,9 +239,9 @@ __global__ void k_crc_finalize(uint32_t* acc, uint32_t k_n, uint64_t count, uint
 void launch_crc_partial(const uint8_t* base, uint64_t stride, uint64_t n, uint64_t count, const CrcTables& ct,
                         uint32_t* acc, cudaStream_t s) {
     if (n == 0 || count == 0) return;
-    const uint64_t chunks = (n + kCrcChunk - 1) / kCrcChunk;
-    const unsigned gx = (unsigned)((chunks + kCrcThreads - 1) / kCrcThreads);
-    k_crc_partial<<<dim3(gx, (unsigned)count), kCrcThreads, 0, s>>>(base, stride, n, ct, acc);
+    const uint64_t segs = (n / 4 + 1 + kSegWords - 1) / kSegWords; // words + the tail
+    const unsigned gx = (unsigned)((segs + kEncWarps - 1) / kEncWarps);
+    k_crc_partial<<<dim3(gx, (unsigned)count), 32 * kEncWarps, 0, s>>>(base, stride, n, ct, acc);
 }
 
 void launch_encode_image_frames(const ImageFrameArgs& a, uint64_t count, const CrcTables& ct, cudaStream_t s) {

@@ -112,7 +112,6 @@ void launch_beamform(const double* filt, double* beams, const int32_t* shifts, i
 double measure_fma_peak(int sms, bool f32);
 
 // ---- wire-format frames on the GPU (frames.cu) ------------------------------
-constexpr int kCrcChunk = 512;      // bytes per thread (multiple of 4)
 constexpr int kCrcShiftMats = 48;   // A_{2^k}, k < 48: messages up to 2^48 bytes
 struct CrcTables {
     const uint32_t* slice;          // [4][256] slicing-by-4 tables
