@@ -466,9 +466,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
                     for (int i = 0; i < 8; ++i)
                         v[i] = i64_ldexp_exact((long long)hi[i0 + i] * 16777216LL + yl[16 * h + i0 + i], eadj);
                     const int64_t n0 = (int64_t)tt * TN + colq * NC + 16 * h + i0;
-#ifdef SNB_TC_NOSTORE
-                    if (n0 >= 0) continue;
-#endif
                     if (a.f32) {
                         float* out = reinterpret_cast<float*>(a.beams) + ((size_t)b * a.n_dirs + slot) * a.N + n0;
                         if (n0 + 8 <= a.L) {
