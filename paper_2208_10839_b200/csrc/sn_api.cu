@@ -576,25 +576,35 @@ struct sn_workspace {
     }
 
     // Enqueue the whole pipeline for `count` measurements (count <= max_batch).
-    void enqueue(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s, bool with_envelope = true) {
+    // Front end (demod, pre-MF FIR, matched filter) of captures
+    // [off, off + count), whose packed bits are at d_in.
+    void enqueue_front(const uint8_t* d_in, uint64_t off, uint64_t count, cudaStream_t s) {
         const Sizes& z = plan.sz;
+        double* dm = d_demod + off * kCh * z.demod_len;
+        double* mf = d_mf + off * kCh * z.mf_fft;
         DemodArgs da = demod;
         da.packed = d_in;
-        da.demod = d_demod;
+        da.demod = dm;
         da.batch = (int)count;
         if (profiling) cudaEventRecord(ev[0], s);
         launch_demod(da, demod_grid, demod_smem, s);
         if (profiling) cudaEventRecord(ev[1], s);
-        PremfArgs pa{d_demod, d_mf, d_premf, (int64_t)z.demod_len, (int64_t)z.mf_len, (int64_t)z.mf_fft,
+        PremfArgs pa{dm, mf, d_premf, (int64_t)z.demod_len, (int64_t)z.mf_len, (int64_t)z.mf_fft,
                      (int)plan.premf_rev.size(), plan.cfg.pre_mf_decimation, plan.premf_rev.data()};
         launch_premf(pa, (int)count, s);
         if (profiling) cudaEventRecord(ev[2], s);
-        MfArgs ma{d_mf, d_filt, f32 && !tc ? d_filt32 : nullptr, d_ref_spec, d_tw_mf,
+        MfArgs ma{mf, d_filt + off * kCh * lp, f32 && !tc ? d_filt32 + off * kCh * lp : nullptr, d_ref_spec, d_tw_mf,
                   (int64_t)z.mf_len, (int64_t)lp, (int64_t)z.mf_fft, (int)z.mf_fft, (int)z.ref_len, halo,
-                  tc ? d_amax : nullptr};
-        if (tc) ck(cudaMemsetAsync(d_amax, 0, count * sizeof(unsigned long long), s), "memset");
+                  tc ? d_amax + off : nullptr};
+        if (tc) ck(cudaMemsetAsync(d_amax + off, 0, count * sizeof(unsigned long long), s), "memset");
         launch_matched_filter(ma, (int)count, mf_smem, s);
         if (profiling) cudaEventRecord(ev[3], s);
+    }
+
+    void enqueue(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s, bool with_envelope = true,
+                 bool with_front = true) {
+        const Sizes& z = plan.sz;
+        if (with_front) enqueue_front(d_in, 0, count, s);
         if (tc) {
             DigitArgs dg{d_filt, d_amax, d_tc_base, d_planes, d_dwords, (int64_t)z.mf_len, (int64_t)lp, halo, tc_rows,
                          tc_pad, tc_clusters};
@@ -709,22 +719,31 @@ struct sn_workspace {
         uint64_t done = 0;
         while (done < count) {
             const uint64_t c = std::min(max_batch, count - done);
-            // all captures up (copy stream), the front end + beamformer for the
-            // whole block, then the envelope in chunks whose energyscapes are
-            // downloaded (D2H stream) while the next chunk computes: only the
-            // upload and the last chunk's download are exposed
-            for (uint64_t i = 0; i < c; ++i) {
-                const uint8_t* src = ms[done + i].packed;
-                if (!is_pinned(src)) {
-                    std::memcpy(h_in + i * packed_bytes, src, packed_bytes);
-                    src = h_in + i * packed_bytes;
+            // captures uploaded in up to 4 parts (copy stream), the front end
+            // of part p running while part p + 1 is on the bus; the
+            // beamformer for the whole block; then the envelope in chunks whose
+            // energyscapes are downloaded (D2H stream) while the next chunk
+            // computes: only the first part's upload and the last chunk's
+            // download are exposed
+            const uint64_t parts = std::min<uint64_t>(c, 4);
+            uint64_t p0 = 0;
+            for (uint64_t p = 0; p < parts; ++p) {
+                const uint64_t p1 = c * (p + 1) / parts;
+                for (uint64_t i = p0; i < p1; ++i) {
+                    const uint8_t* src = ms[done + i].packed;
+                    if (!is_pinned(src)) {
+                        std::memcpy(h_in + i * packed_bytes, src, packed_bytes);
+                        src = h_in + i * packed_bytes;
+                    }
+                    ck(cudaMemcpyAsync(d_packed + i * packed_bytes, src, packed_bytes, cudaMemcpyHostToDevice, s_h2d),
+                       "H2D");
                 }
-                ck(cudaMemcpyAsync(d_packed + i * packed_bytes, src, packed_bytes, cudaMemcpyHostToDevice, s_h2d),
-                   "H2D");
+                ck(cudaEventRecord(ev_in[p], s_h2d), "event");
+                ck(cudaStreamWaitEvent(stream, ev_in[p], 0), "wait");
+                enqueue_front(d_packed + p0 * packed_bytes, p0, p1 - p0, stream);
+                p0 = p1;
             }
-            ck(cudaEventRecord(ev_in[0], s_h2d), "event");
-            ck(cudaStreamWaitEvent(stream, ev_in[0], 0), "wait");
-            enqueue(d_packed, c, d_energy, stream, /*with_envelope=*/false);
+            enqueue(d_packed, c, d_energy, stream, /*with_envelope=*/false, /*with_front=*/false);
             const std::vector<uint64_t> chunks = env_chunks(c);
             const uint64_t nch = chunks.size();
             uint64_t off = 0;
@@ -739,7 +758,7 @@ struct sn_workspace {
                 off += k;
             }
             ck(cudaGetLastError(), "kernel launch");
-            last_launches = (tc ? 6 : 4) + nch;
+            last_launches = 3 * parts + (tc ? 3 : 1) + nch;
             ck(cudaStreamSynchronize(s_d2h), "process sync");
             if (!out_pinned) std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
             done += c;
