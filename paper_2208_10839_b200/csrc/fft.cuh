@@ -345,77 +345,121 @@ __device__ __forceinline__ void hilbert_spectral(V* buf, int M, const TW& tw, R 
     gsync();
 }
 
-// The middle of the Hilbert transform for M = 4096 (= kGroupThreads radix-16
-// butterflies per pass), entirely in registers: the last forward pass, the
-// Hilbert operator of hilbert_spectral and the first inverse pass, replacing
-// two shared-memory round trips and two barriers with a warp shuffle.
-// Butterfly j of the last forward pass yields Z[j + 256 S], S = 0..15; the
-// complementary bins M - j - 256 S = (256 - j) + 256 (15 - S) all belong to
-// butterfly 256 - j, so butterflies j and 256 - j are placed on lanes l and
-// l + 16 of one warp (j = 0 and j = 128 pair with themselves), exchange with
-// __shfl_xor(16), and each applies the operator to its own 16 bins; those are
-// exactly the inputs of inverse butterfly j (ns = 1). Twiddles of the
-// operator: e^{-i t_k}, t_k = t_j + 2 pi S / 32, by angle addition from one
-// table value per thread.
+// cos(k pi / 16) as exact literals (twiddles of the Hilbert operator)
 __device__ __forceinline__ constexpr double cos_pi16(int k) { // cos(k pi / 16), k in [0, 8]
     return k == 0 ? 1.0 : k == 1 ? 0.98078528040323044913 : k == 2 ? 0.92387953251128675613
          : k == 3 ? 0.83146961230254523708 : k == 4 ? 0.70710678118654752440 : k == 5 ? 0.55557023301960222474
          : k == 6 ? 0.38268343236508977173 : k == 7 ? 0.19509032201612826785 : 0.0;
 }
-template <typename V> __device__ __forceinline__ V shfl_xor16(V v) {
-    return V{__shfl_xor_sync(0xffffffffu, v.x, 16), __shfl_xor_sync(0xffffffffu, v.y, 16)};
+
+// ---------------------------------------------------------------------------
+// In-place M = 4096 transform pair for the Hilbert envelope (3 radix-16
+// passes each way, one butterfly per thread): every pass after the first
+// loads and stores the SAME 16 positions, so no barrier is needed between a
+// pass's loads and its stores (the Stockham passes above need one).
+// Forward: decimation in frequency, natural input, output digit-reversed:
+//   position 256 k1 + 16 k2 + k3 holds X[k1 + 16 k2 + 256 k3].
+// Inverse: decimation in time from that digit-reversed order, natural output.
+// Index digits: n = 256 n1 + 16 n2 + n3, k = k1 + 16 k2 + 256 k3.
+// ---------------------------------------------------------------------------
+// the 15 twiddle powers w^e, e = 1..15, from w^1, w^2, w^4, w^8 (4 table loads)
+template <typename V, typename TW>
+__device__ __forceinline__ void tw_powers(const TW& tw, int ns, int k, V (&w)[16]) {
+    w[1] = tw.w(4096, ns, 16, k, 1);
+    w[2] = tw.w(4096, ns, 16, k, 2);
+    w[4] = tw.w(4096, ns, 16, k, 4);
+    w[8] = tw.w(4096, ns, 16, k, 8);
+    w[3] = cmul(w[1], w[2]);
+    w[5] = cmul(w[1], w[4]);
+    w[6] = cmul(w[2], w[4]);
+    w[7] = cmul(w[3], w[4]);
+#pragma unroll
+    for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
 }
 
+// forward pass 1: v[r] = x[j + 256 r] (j = gtid()); A[k1][j] = DFT16_n1 * W4096^{j k1}
+// stored at j + 256 k1
+template <typename V, typename TW>
+__device__ __forceinline__ void dif_pass1_4096(V (&v)[16], V* buf, const TW& tw) {
+    const int j = gtid();
+    dft16<false>(v);
+    V w[16];
+    tw_powers(tw, 256, j, w);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const int k1 = out_slot<16>(r);
+        const V y = k1 ? cmul(v[r], w[k1 ? k1 : 1]) : v[r];
+        buf[pad16(j + 256 * k1)] = y;
+    }
+    gsync();
+}
+
+// forward pass 2 (thread (k1, n3)): DFT16 over n2, * W256^{n3 k2}, in place
+template <typename V, typename TW>
+__device__ __forceinline__ void dif_pass2_4096(V* buf, const TW& tw) {
+    const int t = gtid(), k1 = t >> 4, n3 = t & 15;
+    V v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = buf[pad16(256 * k1 + 16 * r + n3)];
+    dft16<false>(v);
+    V w[16];
+    tw_powers(tw, 16, n3, w);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const int k2 = out_slot<16>(r);
+        const V y = k2 ? cmul(v[r], w[k2 ? k2 : 1]) : v[r];
+        buf[pad16(256 * k1 + 16 * k2 + n3)] = y;
+    }
+    gsync();
+}
+
+// Forward pass 3 + the Hilbert operator + inverse stage A, in registers and in
+// place. Thread (k1, k2), a = k1 + 16 k2, holds X[a + 256 k3], k3 = 0..15; the
+// complementary bins M - a - 256 k3 = (256 - a) + 256 (15 - k3) belong to
+// thread 256 - a: lanes l < 16 of warp w < 7 take k1 = w + 1, k2 = l, lanes
+// l + 16 the partner (k1 = 15 - w, k2 = 15 - l); warp 7 holds k1 = 0 (lanes
+// 0-15) and k1 = 8 (lanes 16-31), partners inside the half-warp (a = 0 and
+// a = 128 pair with themselves). Row 16 k1 + k2 of the padded buffer differs
+// mod 8 within every quarter-warp: conflict-free 16-byte accesses.
 template <typename V, typename TW, typename R>
-__device__ __forceinline__ void hilbert_mid_4096(V* buf, const TW& tw, R s) {
-    constexpr int M = 4096, NS = M / 16;
-    static_assert(NS == kGroupThreads, "one butterfly per thread");
-    const int t = gtid(), l = t & 31;
-    const int m = 16 * (t >> 5) + (l & 15);
-    const int j = l < 16 ? m : (m == 0 ? NS / 2 : NS - m);
-    const bool self0 = t == 0, self_half = t == 16; // j = 0, j = 128
-    // last forward pass (radix 16, ns = 256), as stockham_pass
+__device__ __forceinline__ void hilbert_mid_dif_4096(V* buf, const TW& tw, R s) {
+    const int t = gtid(), w = t >> 5, l = t & 31;
+    int k1, k2, src;
+    if (w < 7) {
+        k1 = l < 16 ? w + 1 : 15 - w;
+        k2 = l < 16 ? l : 31 - l;
+        src = l ^ 16;
+    } else {
+        k1 = l < 16 ? 0 : 8;
+        k2 = l & 15;
+        src = l < 16 ? ((16 - l) & 15) : 47 - l;
+    }
+    const int a = k1 + 16 * k2, row = 256 * k1 + 16 * k2;
+    const bool self0 = a == 0;
     V z[16];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) z[r] = buf[pad16(j + r * NS)];
-    {
-        V w[16];
-        w[1] = tw.w(M, NS, 16, j, 1);
-        w[2] = tw.w(M, NS, 16, j, 2);
-        w[4] = tw.w(M, NS, 16, j, 4);
-        w[8] = tw.w(M, NS, 16, j, 8);
-        w[3] = cmul(w[1], w[2]);
-        w[5] = cmul(w[1], w[4]);
-        w[6] = cmul(w[2], w[4]);
-        w[7] = cmul(w[3], w[4]);
-#pragma unroll
-        for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
-#pragma unroll
-        for (int r = 1; r < 16; ++r) z[r] = cmul(z[r], w[r]);
-    }
-    dft16<false>(z); // z[out_slot(S)] = Z[j + 256 S]
-    const V hj = tw.h(j);
-    const R cj = s * hj.x, sj = -s * hj.y; // s (cos t_j, sin t_j), s a power of two
-    auto cosS = [](int S) { return (R)(S <= 8 ? cos_pi16(S) : -cos_pi16(16 - S)); }; // cos(2 pi S / 32)
+    for (int r = 0; r < 16; ++r) z[r] = buf[pad16(row + r)];
+    dft16<false>(z); // z[out_slot(S)] = X[a + 256 S]
+    const V ha = tw.h(a);
+    const R cj = s * ha.x, sj = -s * ha.y;
+    auto cosS = [](int S) { return (R)(S <= 8 ? cos_pi16(S) : -cos_pi16(16 - S)); };
     auto sinS = [](int S) { return (R)cos_pi16(S <= 8 ? 8 - S : S - 8); };
-    // Z'[k] = s (cos t_k conj(Z[M-k]) + i sin t_k Z[k])
     auto op = [&](V zk, V zc, int S) {
         const R c = cj * cosS(S) - sj * sinS(S), sn = sj * cosS(S) + cj * sinS(S);
         return V{c * zc.x - sn * zk.y, sn * zk.x - c * zc.y};
     };
+    auto shfl = [&](V v) {
+        return V{__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src)};
+    };
 #pragma unroll
     for (int S = 0; S < 8; ++S) {
-        V& a = z[out_slot<16>(S)];
-        V& b = z[out_slot<16>(15 - S)];
-        V pa = shfl_xor16(b), pb = shfl_xor16(a); // partner's Z[15 - S], Z[S]
-        if (self_half) {
-            pa = b;
-            pb = a;
-        }
+        V& x0 = z[out_slot<16>(S)];
+        V& x1 = z[out_slot<16>(15 - S)];
+        const V pa = shfl(x1), pb = shfl(x0); // partner's X[. + 256 (15 - S)], X[. + 256 S]
         if (!self0) {
-            const V na = op(a, pa, S), nb = op(b, pb, 15 - S);
-            a = na;
-            b = nb;
+            const V n0 = op(x0, pa, S), n1 = op(x1, pb, 15 - S);
+            x0 = n0;
+            x1 = n1;
         }
     }
     if (self0) {
@@ -423,35 +467,58 @@ __device__ __forceinline__ void hilbert_mid_4096(V* buf, const TW& tw, R s) {
         z[0] = V{(R)0, (R)0};
 #pragma unroll
         for (int S = 1; S <= 8; ++S) {
-            V& a = z[out_slot<16>(S)];
-            V& b = z[out_slot<16>(16 - S)];
-            const V na = op(a, b, S), nb = op(b, a, 16 - S);
-            a = na;
-            if (S != 8) b = nb;
+            V& x0 = z[out_slot<16>(S)];
+            V& x1 = z[out_slot<16>(16 - S)];
+            const V n0 = op(x0, x1, S), n1 = op(x1, x0, 16 - S);
+            x0 = n0;
+            if (S != 8) x1 = n1;
         }
     }
-    // first inverse pass (radix 16, ns = 1): inputs Z'[j + 256 r]
+    // inverse stage A: DFT16 over k3 of Z'[a + 256 k3] -> A[k1][k2][n3], stored
+    // in place (this thread's own row: no barrier before the stores)
     V x[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) x[r] = z[out_slot<16>(r)];
     dft16<true>(x);
-    gsync(); // every thread's forward-pass loads are done
 #pragma unroll
-    for (int r = 0; r < 16; ++r) buf[pad16(16 * j + out_slot<16>(r))] = x[r];
+    for (int r = 0; r < 16; ++r) buf[pad16(row + out_slot<16>(r))] = x[r];
     gsync();
 }
 
-// First pass (radix 16, ns = 1) of an M = 16 * kGroupThreads transform from
-// inputs already in registers (v[r] = x[gtid() + r * M / 16]), so that the
-// caller can issue the global loads early (e.g. before the previous item's
-// tail work).
-template <bool INV, typename V>
-__device__ __forceinline__ void first_pass_from_regs(V (&v)[16], V* dst) {
-    dft16<INV>(v);
-    const int base = 16 * gtid();
+// inverse stage B (thread (k1, n3)): * conj W256^{k2 n3}, DFT16 over k2, in place
+template <typename V, typename TW>
+__device__ __forceinline__ void dit_pass2_4096(V* buf, const TW& tw) {
+    const int t = gtid(), k1 = t >> 4, n3 = t & 15;
+    V v[16];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) dst[pad16(base + out_slot<16>(r))] = v[r];
+    for (int r = 0; r < 16; ++r) v[r] = buf[pad16(256 * k1 + 16 * r + n3)];
+    V w[16];
+    tw_powers(tw, 16, n3, w);
+#pragma unroll
+    for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], cconj(w[r]));
+    dft16<true>(v);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[pad16(256 * k1 + 16 * out_slot<16>(r) + n3)] = v[r];
     gsync();
+}
+
+// inverse stage C (thread m = n3 + 16 n2): * conj W4096^{k1 m}, DFT16 over k1;
+// output z[m + 256 n1] (natural order) handed to sink(n, value) after a
+// barrier (the sink may overwrite the buffer)
+template <typename V, typename TW, typename Sink>
+__device__ __forceinline__ void dit_pass3_4096(V* buf, const TW& tw, Sink sink) {
+    const int m = gtid();
+    V v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = buf[pad16(256 * r + m)];
+    V w[16];
+    tw_powers(tw, 256, m, w);
+#pragma unroll
+    for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], cconj(w[r]));
+    dft16<true>(v);
+    gsync();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) sink(m + 256 * out_slot<16>(r), v[r]);
 }
 
 } // namespace snb

@@ -489,9 +489,9 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
         if constexpr (M == 4096) {
 #pragma unroll
             for (int r = kPre; r < 16; ++r) pre[r] = __ldg(reinterpret_cast<const V*>(src) + tid + r * kGroupThreads);
-            first_pass_from_regs<false>(pre, bufB);
-            stockham_pass<16, false, true, M>(bufB, bufB, 16, twsrc);
-            hilbert_mid_4096(bufB, twsrc, scale);
+            dif_pass1_4096(pre, bufB, twsrc);
+            dif_pass2_4096(bufB, twsrc);
+            hilbert_mid_dif_4096(bufB, twsrc, scale);
         } else {
             cfft<M, false, false>(reinterpret_cast<const V*>(src), bufB, twsrc);
             hilbert_spectral(bufB, M, twsrc, scale);
@@ -519,8 +519,8 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
                 if (2 * n + 1 < Li) ph[pp + 1 == D ? u + 1 : (pp + 1) * PL + u] = m1;
             };
             if constexpr (M == 4096) {
-                stockham_pass<16, true, true, M>(bufB, bufB, 16, twsrc);
-                stockham_pass<16, true, true, M>(bufB, bufB, 256, twsrc, sink);
+                dit_pass2_4096(bufB, twsrc);
+                dit_pass3_4096(bufB, twsrc, sink);
             } else {
                 cfft<M, true, true>(bufB, bufB, twsrc, sink);
             }
