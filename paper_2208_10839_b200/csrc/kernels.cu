@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
 #ifndef SNB_PRE
 #define SNB_PRE 2
 #endif
-    constexpr int kPre = SNB_PRE; // of the 16 inputs per thread: measured best at 2 (0: 3.71 ms, 1: 3.61, 2: 3.59, 3: 3.66, 4: 3.71, 8+: spills)
+    constexpr int kPre = SNB_PRE; // of the 16 inputs per thread; envelope ms by depth 0-4: 3.56, 3.48, 3.48, 3.60, 3.59 (8+: spills)
     V pre[16];
     auto load_pre = [&](int64_t item) {
         const V* s = reinterpret_cast<const V*>(a.beams) + (size_t)item * M;
