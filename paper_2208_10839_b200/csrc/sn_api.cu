@@ -117,6 +117,10 @@ struct sn_workspace {
     // host path: copies run on their own streams so that chunk j+1's H2D and
     // chunk j-1's D2H overlap chunk j's kernels
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    // second compute stream: envelope chunks alternate between `stream` and
+    // s_env2 so that a chunk's CTAs fill the SMs its predecessor's tail frees
+    cudaStream_t s_env2 = nullptr;
+    cudaEvent_t ev_beams = nullptr;
     static constexpr int kMaxChunks = 16;
     // envelope chunk sizes of a block of c captures: ~2 per chunk, the last
     // chunk a single capture (its download is the exposed one)
@@ -221,6 +225,8 @@ struct sn_workspace {
         }
         if (s_h2d) cudaStreamDestroy(s_h2d);
         if (s_d2h) cudaStreamDestroy(s_d2h);
+        if (s_env2) cudaStreamDestroy(s_env2);
+        if (ev_beams) cudaEventDestroy(ev_beams);
         for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
                         (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot,  (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
@@ -254,6 +260,8 @@ struct sn_workspace {
         ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&s_env2, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaEventCreateWithFlags(&ev_beams, cudaEventDisableTiming), "cudaEventCreate");
         for (int j = 0; j < kMaxChunks; ++j) {
             ck(cudaEventCreateWithFlags(&ev_in[j], cudaEventDisableTiming), "cudaEventCreate");
             ck(cudaEventCreateWithFlags(&ev_done[j], cudaEventDisableTiming), "cudaEventCreate");
@@ -744,13 +752,16 @@ struct sn_workspace {
                 p0 = p1;
             }
             enqueue(d_packed, c, d_energy, stream, /*with_envelope=*/false, /*with_front=*/false);
+            ck(cudaEventRecord(ev_beams, stream), "event");
+            ck(cudaStreamWaitEvent(s_env2, ev_beams, 0), "wait");
             const std::vector<uint64_t> chunks = env_chunks(c);
             const uint64_t nch = chunks.size();
             uint64_t off = 0;
             for (uint64_t j = 0; j < nch; ++j) {
                 const uint64_t k = chunks[j]; // captures in chunk j
-                enqueue_envelope(off, k, d_energy + off * energy_per, stream);
-                ck(cudaEventRecord(ev_done[j], stream), "event");
+                cudaStream_t cs = (j & 1) ? s_env2 : stream;
+                enqueue_envelope(off, k, d_energy + off * energy_per, cs);
+                ck(cudaEventRecord(ev_done[j], cs), "event");
                 ck(cudaStreamWaitEvent(s_d2h, ev_done[j], 0), "wait");
                 float* dst = (out_pinned ? out + done * energy_per : h_out) + off * energy_per;
                 ck(cudaMemcpyAsync(dst, d_energy + off * energy_per, k * energy_per * sizeof(float),
@@ -833,16 +844,19 @@ struct sn_workspace {
             const std::vector<uint64_t> chunks = env_chunks(c);
             const uint64_t nch = chunks.size();
             uint64_t off = 0;
+            ck(cudaEventRecord(ev_beams, stream), "event");
+            ck(cudaStreamWaitEvent(s_env2, ev_beams, 0), "wait");
             for (uint64_t j = 0; j < nch; ++j) {
                 const uint64_t k = chunks[j];
-                enqueue_envelope(off, k, d_energy + off * energy_per, stream);
+                cudaStream_t cs = (j & 1) ? s_env2 : stream;
+                enqueue_envelope(off, k, d_energy + off * energy_per, cs);
                 ImageFrameArgs ia{d_energy + off * energy_per, d_img_tpl, d_ids + off,
                                   d_frames_out + off * img_frame_stride, d_crc_acc + max_batch + off, energy_per,
                                   img_tpl_len, img_frame_len, img_frame_stride};
-                launch_encode_image_frames(ia, k, ct, stream);
+                launch_encode_image_frames(ia, k, ct, cs);
                 launch_crc_finalize(d_crc_acc + max_batch + off, kout, k, d_frames_out + off * img_frame_stride,
-                                    img_frame_stride, nout, true, nullptr, stream);
-                ck(cudaEventRecord(ev_done[j], stream), "event");
+                                    img_frame_stride, nout, true, nullptr, cs);
+                ck(cudaEventRecord(ev_done[j], cs), "event");
                 ck(cudaStreamWaitEvent(s_d2h, ev_done[j], 0), "wait");
                 uint8_t* dst = direct ? out + (batch.front() + off) * slot : h_frames_out + off * img_frame_len;
                 const uint64_t dpitch = direct ? slot : img_frame_len;
