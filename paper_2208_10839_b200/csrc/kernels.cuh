@@ -150,6 +150,7 @@ struct SynthArgs {
     const double* pulse;        // PDM-rate pulse (ref_len)
     const SynthScene* scenes;   // [count]
     uint32_t* words;            // [count][32][nwords] scratch
+    unsigned long long* states; // [count][32][4] noise-stream state at each channel start (scratch)
     uint8_t* packed;            // [count][packed_bytes]
     int64_t frames, ref_len, nwords, packed_bytes;
     int count;

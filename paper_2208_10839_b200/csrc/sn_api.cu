@@ -1309,15 +1309,18 @@ sn_status sn_synthesize_device(const sn_pipeline_config* cfg, const sn_scene* sc
         double* d_pulse = nullptr;
         SynthScene* d_sc = nullptr;
         uint32_t* d_words = nullptr;
+        unsigned long long* d_states = nullptr;
+        ck(cudaMallocAsync(&d_states, count * kCh * 4 * sizeof(unsigned long long), st), "cudaMallocAsync");
         ck(cudaMallocAsync(&d_pulse, pulse.size() * sizeof(double), st), "cudaMallocAsync");
         ck(cudaMallocAsync(&d_sc, count * sizeof(SynthScene), st), "cudaMallocAsync");
         ck(cudaMallocAsync(&d_words, count * 32 * nwords * sizeof(uint32_t), st), "cudaMallocAsync");
         ck(cudaMemcpyAsync(d_pulse, pulse.data(), pulse.size() * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
         ck(cudaMemcpyAsync(d_sc, sc.data(), count * sizeof(SynthScene), cudaMemcpyHostToDevice, st), "H2D");
-        SynthArgs a{d_pulse, d_sc, d_words, d_packed, (int64_t)frames, (int64_t)pulse.size(), nwords,
+        SynthArgs a{d_pulse, d_sc, d_words, d_states, d_packed, (int64_t)frames, (int64_t)pulse.size(), nwords,
                     (int64_t)(kCh * frames / 8), (int)count};
         launch_synth(a, st);
         ck(cudaGetLastError(), "synth launch");
+        cudaFreeAsync(d_states, st);
         cudaFreeAsync(d_pulse, st);
         cudaFreeAsync(d_sc, st);
         cudaFreeAsync(d_words, st);

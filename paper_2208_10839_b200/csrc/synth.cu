@@ -5,11 +5,17 @@
 // noise from one xoshiro256++ stream in channel-major sample order with the
 // polar Box-Muller method and its cached spare (rng.hpp), the first-order
 // sigma-delta modulator per channel (:63-94) and frame-major MSB-first packing
-// (:96-114). The noise stream and the modulator are sequential by definition
-// (the Box-Muller rejection makes the stream position of every sample data
-// dependent), so one thread runs one capture end to end and a batch of
-// captures runs in parallel; the FP64 operations are issued in the
-// reference's order without contraction (__dadd_rn / __dmul_rn). Echo
+// (:96-114). The noise stream is sequential by definition (the Box-Muller
+// rejection makes the stream position of every sample data dependent), but
+// its expensive part is not: k_synth_skip walks each capture's stream once
+// with only the cheap acceptance test (two draws, q = u^2 + v^2, the same
+// rounded operations) and records the generator state at every channel
+// start; k_synth_sd then runs one thread per (capture, channel) with the
+// logarithm, square root and the sigma-delta modulator. With an even frame
+// count every channel consumes whole accepted pairs, so no cached spare
+// crosses a channel boundary (odd frame counts run the whole capture in one
+// thread). The FP64 operations are issued in the reference's order without
+// contraction (__dadd_rn / __dmul_rn). Echo
 // geometry (pulse, amplitudes, onsets) comes from the host planner
 // (plan.cpp scene_echoes), so it is the reference's to the bit. log() on the
 // device may differ from the host's in the last place; a sigma-delta decision
@@ -70,16 +76,36 @@ struct DevRng {
 
 } // namespace
 
-// One thread per capture: echoes + noise + sigma-delta, channel by channel;
-// bits land channel-major in words[capture][32][nwords] (bit i of word w =
-// frame 32 w + i).
-__global__ void k_synth_sd(SynthArgs a) {
+// Generator state at the start of every channel: frames / 2 accepted pairs
+// per channel (even frame count), rejections included.
+__global__ void k_synth_skip(SynthArgs a) {
     const int cap = blockIdx.x * blockDim.x + threadIdx.x;
     if (cap >= a.count) return;
     const SynthScene sc = a.scenes[cap];
     DevRng rng(sc.seed);
-    uint32_t* words = a.words + (size_t)cap * 32 * a.nwords;
+    unsigned long long* st = a.states + (size_t)cap * 32 * 4;
+    const int64_t pairs = a.frames / 2;
     for (int ch = 0; ch < 32; ++ch) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) st[4 * ch + k] = rng.s[k];
+        if (sc.noise_rms <= 0.0) continue;
+        for (int64_t i = 0; i < pairs; ++i) {
+            double q;
+            do {
+                const double u = __dsub_rn(__dmul_rn(2.0, rng.uniform()), 1.0);
+                const double v = __dsub_rn(__dmul_rn(2.0, rng.uniform()), 1.0);
+                q = __dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v));
+            } while (q >= 1.0 || q == 0.0);
+        }
+    }
+}
+
+// Echoes + noise + sigma-delta for channels [ch0, ch1) of a capture, starting
+// from the generator state `rng`; bits land channel-major in
+// words[capture][32][nwords] (bit i of word w = frame 32 w + i).
+__device__ void synth_channels(const SynthArgs& a, const SynthScene& sc, DevRng& rng, int cap, int ch0, int ch1) {
+    uint32_t* words = a.words + (size_t)cap * 32 * a.nwords;
+    for (int ch = ch0; ch < ch1; ++ch) {
         double integ = 0.0;
         uint32_t w = 0;
         for (int64_t i = 0; i < a.frames; ++i) {
@@ -99,6 +125,28 @@ __global__ void k_synth_sd(SynthArgs a) {
             }
         }
     }
+}
+
+// one thread per (capture, channel), from the recorded channel-start states
+__global__ void k_synth_sd(SynthArgs a) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)a.count * 32) return;
+    const int cap = (int)(t / 32), ch = (int)(t % 32);
+    const SynthScene sc = a.scenes[cap];
+    DevRng rng(0);
+    const unsigned long long* st = a.states + ((size_t)cap * 32 + ch) * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rng.s[k] = st[k];
+    synth_channels(a, sc, rng, cap, ch, ch + 1);
+}
+
+// odd frame counts: one thread per capture, all channels in stream order
+__global__ void k_synth_sd_serial(SynthArgs a) {
+    const int cap = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cap >= a.count) return;
+    const SynthScene sc = a.scenes[cap];
+    DevRng rng(sc.seed);
+    synth_channels(a, sc, rng, cap, 0, 32);
 }
 
 // Channel-major bit words -> frame-major packed bytes (pack_pdm, synth.cpp:
@@ -122,7 +170,12 @@ __global__ void k_synth_pack(SynthArgs a) {
 }
 
 void launch_synth(const SynthArgs& a, cudaStream_t s) {
-    k_synth_sd<<<(a.count + 31) / 32, 32, 0, s>>>(a);
+    if (a.frames % 2 == 0) {
+        k_synth_skip<<<(a.count + 31) / 32, 32, 0, s>>>(a);
+        k_synth_sd<<<(unsigned)((a.count * 32 + 31) / 32), 32, 0, s>>>(a);
+    } else {
+        k_synth_sd_serial<<<(a.count + 31) / 32, 32, 0, s>>>(a);
+    }
     const int64_t warps = (int64_t)a.count * a.nwords;
     k_synth_pack<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(a);
 }
