@@ -23,9 +23,8 @@ namespace snb {
 // r = m mod P shares the bit alignment a = s & 7, so a CTA serves one class
 // and keeps that alignment's 33 x 256 FP64 table (67.6 KB) in shared memory
 // for its whole life (persistent grid over (measurement, block of m)).
-// Frames are transposed into per-channel MSB-first rows with warp ballots:
-// lane l holds frame word l, ballot over channel c's bit yields 32 frames of
-// channel c. The sum per output follows the reference exactly: four lanes
+// Frames are transposed into per-channel MSB-first rows by a 32 x 32 bit
+// transpose across the warp (lane l holds frame word l; 5 shuffle stages). The sum per output follows the reference exactly: four lanes
 // over octets t = 0 .. 4*floor(T/4)-1 (lane t mod 4), (a0+a1)+(a2+a3), then
 // the remaining octets in order; adds only, every add rounded (DADD).
 // ---------------------------------------------------------------------------
@@ -68,15 +67,25 @@ __global__ void __launch_bounds__(kThreads) k_demod(DemodArgs a) {
             for (int g = warp; g < nwords && g < a.words; g += nwarps) {
                 const int64_t f = F0 + 32 * (int64_t)g + lane;
                 const uint32_t w = f < a.frames ? *reinterpret_cast<const uint32_t*>(pk + 4 * f) : 0u;
-                uint32_t mine = 0;
-#pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    // channel c: byte c/8 of the frame word, bit 7 - c%8 (MSB first)
-                    const uint32_t m = __ballot_sync(0xffffffffu, (w >> ((c & ~7) + 7 - (c & 7))) & 1u);
-                    if (lane == c) mine = m;
-                }
-                // bit f of `mine` = frame F0+32g+f; row bytes are MSB-first per 8 frames
-                rows[lane * a.words + g] = __byte_perm(__brev(mine), 0, 0x0123);
+                // 32 x 32 bit transpose across the warp (5 shuffle stages):
+                // lane c ends with channel c's bits of the 32 frames. Channel c
+                // is bit 7 - c%8 of byte c/8 of a frame word (MSB first); with
+                // the byte-swapped word as input, the transpose leaves frame f
+                // at bit 31 - f of lane c, and the byte-swapped result is the
+                // MSB-first row word (frames 8b..8b+7 in byte b, first frame in
+                // the top bit).
+                uint32_t x = __byte_perm(w, 0, 0x0123);
+                auto stage = [&](int j, uint32_t m) {
+                    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+                    if (lane & j) x ^= ((y ^ (x >> j)) & m) << j;
+                    else x ^= (x ^ (y >> j)) & m;
+                };
+                stage(16, 0x0000FFFFu);
+                stage(8, 0x00FF00FFu);
+                stage(4, 0x0F0F0F0Fu);
+                stage(2, 0x33333333u);
+                stage(1, 0x55555555u);
+                rows[lane * a.words + g] = __byte_perm(x, 0, 0x0123);
             }
         }
         __syncthreads();
