@@ -358,16 +358,42 @@ struct sn_workspace {
         demod.center = (plan.cfg.demod_taps - 1) / 2;
         demod.octets = (int)s.lut_octets;
         demod.period = P;
-        demod.jblock = 64;
-        int words = (int)((int64_t)D * P * (demod.jblock - 1) + demod.taps + 62) / 32 + 3;
-        if (words % 2 == 0) ++words;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        // outputs of one residue class per work item: among the candidates
+        // that keep the most CTAs per SM (LUT + staged rows in shared
+        // memory), the one with the fewest estimated item-waves x (block +
+        // staging margin) for a full batch (hemisphere3000: 48 -> 0.160 ms;
+        // 64 -> 0.221 ms at 2 CTAs/SM; 32 -> 0.170 ms)
+        auto words_for = [&](int jb) {
+            int w = (int)((int64_t)D * P * (jb - 1) + demod.taps + 62) / 32 + 3;
+            return w % 2 == 0 ? w + 1 : w;
+        };
+        auto per_sm_for = [&](int jb) {
+            return std::max(1, (int)((228 * 1024) / (demod_smem_bytes(demod.octets, words_for(jb)) + 1024)));
+        };
+        const int64_t Jr = ((int64_t)s.demod_len + P - 1) / P;
+        const int cands[] = {64, 56, 48, 40, 32, 24};
+        int max_per = 1;
+        for (int jb : cands) max_per = std::max(max_per, per_sm_for(jb));
+        double best = 1e300;
+        demod.jblock = 32;
+        for (int jb : cands) {
+            if (per_sm_for(jb) != max_per) continue;
+            const int64_t grid = std::max(1, sms * max_per / P);
+            const int64_t items = (Jr + jb - 1) / jb * (int64_t)max_batch;
+            const double cost = (double)((items + grid - 1) / grid) * (jb + (double)demod.taps / (D * P));
+            if (cost < best - 1e-9) {
+                best = cost;
+                demod.jblock = jb;
+            }
+        }
+        const int words = words_for(demod.jblock);
         demod.words = words;
         demod_smem = demod_smem_bytes(demod.octets, words);
         if (demod_smem > 227 * 1024) {
             config_error("pipeline: demod taps " + std::to_string(demod.taps) + " exceed the shared-memory LUT limit");
         }
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const int per_sm = std::max(1, (int)((228 * 1024) / (demod_smem + 1024)));
         demod_grid = std::max(1, sms * per_sm / P);
         // beamformer time tile: 32 x (T + 2H) samples staged per CTA
