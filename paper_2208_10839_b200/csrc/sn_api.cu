@@ -506,7 +506,6 @@ struct sn_workspace {
         tc = !(env && std::string(env) == "tiles");
         if (!tc) return;
         const Sizes& s = plan.sz;
-        const uint64_t nd = s.n_dirs;
         tc_R.clear();
         tc_base.clear();
         tc_start.clear();
