@@ -182,7 +182,7 @@ def workload_desc(grid, d, B, pool):
 
 
 # ---------------------------------------------------------------------------
-def cpu_baseline(cfg_b200, grid, calls):
+def cpu_baseline(cfg_b200, grid, calls, warmup=1):
     """Reference C++ core (oracle/_ref, reference Release flags) on all host
     threads: one Workspace per thread, processing_threads=1 (central-node
     model, central_node.cpp:48-53)."""
@@ -196,6 +196,8 @@ def cpu_baseline(cfg_b200, grid, calls):
     rc = rc.copy(processing_threads=1)
     pool = np.stack([ref.synthesize(rc, BENCH_SCENE, 0.01, 7 + s) for s in range(4)])
     threads = os.cpu_count() or 1
+    if warmup > 1:
+        ref.throughput(rc, pool, threads, warmup - 1)  # untimed; the timed run warms up once more
     elapsed, total = ref.throughput(rc, pool, threads, calls)
     return {
         "value": total / elapsed, "unit": UNIT, "cores": threads, "kind": "reference",
@@ -209,16 +211,18 @@ def run_reference(args):
     """Reference arm: the reference's own CPU implementation (oracle/_ref,
     unmodified core sources) on all host threads of this box. One step = every
     host thread runs one process() call on its own Workspace; K is capped at
-    30 steps so the arm stays within a few minutes at hemisphere3000."""
+    30 steps and W at 5 so the arm stays within a few minutes at
+    hemisphere3000."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     steps = max(1, min(args.steps, 30))
-    base = cpu_baseline(None, args.grid, steps)
+    warmup = max(1, min(args.warmup, 5))
+    base = cpu_baseline(None, args.grid, steps, warmup)
     threads = base["cores"]
     line = {
         "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": 1,
+        "steps": steps, "warmup": warmup,
         "ms_per_step": 1e3 * threads / base["value"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference synthesize_measurement, bench scene, seeds 7..10)",
