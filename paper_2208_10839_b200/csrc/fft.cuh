@@ -521,4 +521,195 @@ __device__ __forceinline__ void dit_pass3_4096(V* buf, const TW& tw, Sink sink) 
     for (int r = 0; r < 16; ++r) sink(m + 256 * out_slot<16>(r), v[r]);
 }
 
+// ---------------------------------------------------------------------------
+// Smoothing FIR by FFT (the composite 447-tap filter at stride 10 of
+// pipeline.cpp:466-468, default shapes). In polyphase form the decimated
+// output is a sum of ten 45-tap correlations,
+//     out[o] = sum_p sum_q G_p[q] E_p[o + q],  E_p[u] = env[10 u - c0 + p],
+// G_p[q] = rev[10 q + p]; with o < bins and q < 45 every index stays below
+// 768 >= bins + 44, so a cyclic length-768 correlation is exact (entries
+// [bins + 44, 768) of a phase only reach discarded outputs; they hold
+// envelope samples or zeros, never garbage).
+// The two samples of one magnitude pair (t = n + c0 odd, t + 1) land in one
+// complex slot: sequence a = (t mod 10 - 1) / 2 carries
+//     c_a[u] = E_{2a+1}[u] + i E_{2a+2}[u]       (a < 4)
+//     c_4[u] = E_9[u]      + i E_0[u + 1]         (phase 0 advanced by one:
+//                                                  its taps delayed by one, cyclically)
+// and for real filters the ten correlations collapse to
+//     out = Re( IDFT768( sum_a C_a U_a ) ),
+//     U_a = (conj Ghat_re - i conj Ghat_im) / 768            (host table)
+// i.e. five forward FFTs, one multiply-accumulate and one inverse FFT:
+// ~180k FP64 operations per beam instead of 655 x 450 = 295k FMAs.
+// 768 = 3 x 16 x 16, in place over the group buffer:
+//   forward (decimation in frequency, natural input): radix 3 over n1
+//   (stride 256), radix 16 over n2 (stride 16), radix 16 over n3; position
+//   256 k1 + 16 k2 + k3 ends up holding C[k1 + 3 k2 + 48 k3];
+//   inverse (decimation in time from that order back to natural order).
+// Slot of (sequence a, position x): a * kFfStride + pad16(x); kFfStride = 5
+// mod 8 so the sink's lanes (a = 0..4 cycling, u advancing every 5 lanes)
+// hit distinct bank groups. Every pass loads and stores the same slots per
+// thread (no barrier between a pass's loads and its stores).
+// ---------------------------------------------------------------------------
+constexpr int kFfL = 768, kFfSeq = 5, kFfThreads = 240; // radix-16 butterflies of the 5 forward FFTs
+constexpr int kFfStride = 821;                           // >= pad16(767) + 1, = 5 mod 8
+constexpr int kFfSlots = 4 * kFfStride + 816;            // complex slots of the FIR layout
+constexpr int kFfU = 16 * kFfThreads;                    // spectrum factors (complex)
+constexpr int kFfW = 512;                                // twiddles: w768^j (j < 256), w256^{n3 k2} (16 x 16)
+__device__ __forceinline__ int ff_slot(int a, int x) { return a * kFfStride + pad16(x); }
+
+// w16^k = w256^{16 k} from the 16 x 16 table w256^{n3 k2} (at 16 k2 + n3),
+// k = q m in {0, 1, 2, 3, 4, 6, 9} (lane-dependent: a table load, not a branch)
+template <typename V>
+__device__ __forceinline__ V w16_pow(const V* w256, int k) { return w256[k == 9 ? 16 * 12 + 12 : 16 * 8 + 2 * k]; }
+
+template <bool INV, typename V>
+__device__ __forceinline__ void dft3(V& x0, V& x1, V& x2) {
+    using R = decltype(V{}.x);
+    constexpr R h = (R)0.86602540378443864676; // sin(2 pi / 3)
+    const V s = cadd(x1, x2);
+    const V t = {x0.x - (R)0.5 * s.x, x0.y - (R)0.5 * s.y};
+    const V d = csub(x1, x2);
+    // forward: (x1 - x2) * (-i h); inverse: (x1 - x2) * (+i h)
+    const V u = INV ? V{-h * d.y, h * d.x} : V{h * d.y, -h * d.x};
+    x0 = cadd(x0, s);
+    x1 = cadd(t, u);
+    x2 = csub(t, u);
+}
+
+// out[o] = max(0, float(r[o])) for o < bins. U: [16][kFfThreads] in the
+// register order of the third forward pass; W: [w768^j, j < 256][w256^{n3 k2}
+// at 16 k2 + n3] (e^{-2 pi i . / n}); both in shared memory.
+template <typename V>
+__device__ __forceinline__ void fir_fft768(V* buf, const V* U, const V* W, float* __restrict__ eo, int bins) {
+    using R = decltype(V{}.x);
+    int t = gtid();
+    // opaque per call: keeps the compiler from hoisting every pass's
+    // (loop-invariant) shared-memory addresses out of the item loop and
+    // spilling them
+    asm volatile("" : "+r"(t));
+    const V* w256 = W + 256;
+    {
+        // forward pass 1: radix 3 over n1, * w768^{j k1}, the five sequences
+        const int j = t;
+        const V w1 = W[j], w2 = cmul(w1, w1);
+#pragma unroll
+        for (int a = 0; a < kFfSeq; ++a) {
+            V x0 = buf[ff_slot(a, j)], x1 = buf[ff_slot(a, j + 256)], x2 = buf[ff_slot(a, j + 512)];
+            dft3<false>(x0, x1, x2);
+            buf[ff_slot(a, j)] = x0;
+            buf[ff_slot(a, j + 256)] = cmul(x1, w1);
+            buf[ff_slot(a, j + 512)] = cmul(x2, w2);
+        }
+    }
+    gsync();
+    if (t < kFfThreads) {
+        // forward pass 2 (thread (a, k1, n3)): DFT16 over n2, * w256^{n3 k2}
+        const int a = t / 48, rem = t - 48 * a, k1 = rem >> 4, n3 = rem & 15;
+        V* s = buf + a * kFfStride;
+        const int b = 256 * k1 + n3;
+        V v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = s[pad16(b + 16 * r)];
+        dft16<false>(v);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int k2 = out_slot<16>(r);
+            s[pad16(b + 16 * k2)] = k2 ? cmul(v[r], w256[16 * k2 + n3]) : v[r];
+        }
+    }
+    gsync();
+    if (t < kFfThreads) {
+        // forward pass 3 (thread (a, k1, k2)): DFT16 over n3, times U_a
+        const int a = t / 48, rem = t - 48 * a;
+        V* s = buf + a * kFfStride;
+        const int b = 16 * rem; // 256 k1 + 16 k2
+        V v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = s[pad16(b + r)];
+        dft16<false>(v);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) s[pad16(b + out_slot<16>(r))] = cmul(v[r], U[r * kFfThreads + t]);
+    }
+    gsync();
+    if (t < 192) {
+        // inverse pass A: DFT16 over k3 of the sum over the five sequences, for
+        // group g = (k1, k2) (positions 16 g + k3), four lanes per group:
+        // lane q takes k3 = q + 4 i, DFT4 over i, * w16^{q m}, exchange
+        // through shared memory (slot 4 q + m), DFT4 over q; output n3 = m + 4 p
+        // at slot m + 4 p. Lanes of a quarter-warp serve 8 different groups
+        // (rows 17 apart): conflict-free.
+        const int l = t & 31, g = 8 * (t >> 5) + (l & 7), q = l >> 3;
+        V* s = buf + pad16(16 * g);
+        V x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            V acc = s[q + 4 * i];
+#pragma unroll
+            for (int a = 1; a < kFfSeq; ++a) acc = cadd(acc, s[a * kFfStride + q + 4 * i]);
+            x[i] = acc;
+        }
+        dft4<true>(x[0], x[1], x[2], x[3]);
+#pragma unroll
+        for (int m = 1; m < 4; ++m) x[m] = cmul(x[m], cconj(w16_pow(w256, q * m)));
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < 4; ++m) s[4 * q + m] = x[m];
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = s[4 * i + q]; // T_i[m = q]
+        dft4<true>(x[0], x[1], x[2], x[3]);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) s[q + 4 * p] = x[p];
+    }
+    gsync();
+    if (t < 192) {
+        // inverse pass B: * conj w256^{n3 k2}, DFT16 over k2 for group
+        // g = (k1, n3) (positions 256 k1 + n3 + 16 k2), four lanes per group as
+        // in pass A
+        const int l = t & 31, g = 8 * (t >> 5) + (l & 7), q = l >> 3;
+        const int n3 = g & 15;
+        V* s = buf + 272 * (g >> 4) + n3; // pad16(256 k1 + 16 k2 + n3) = 272 k1 + 17 k2 + n3
+        auto at = [&](int k2) -> V& { return s[17 * k2]; };
+        V x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int k2 = q + 4 * i;
+            x[i] = k2 ? cmul(at(k2), cconj(w256[16 * k2 + n3])) : at(k2);
+        }
+        dft4<true>(x[0], x[1], x[2], x[3]);
+#pragma unroll
+        for (int m = 1; m < 4; ++m) x[m] = cmul(x[m], cconj(w16_pow(w256, q * m)));
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < 4; ++m) at(4 * q + m) = x[m];
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = at(4 * i + q);
+        dft4<true>(x[0], x[1], x[2], x[3]);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) at(q + 4 * p) = x[p];
+    }
+    gsync();
+    {
+        // inverse pass C (thread j = 16 n2 + n3): * conj w768^{j k1}, radix 3
+        // over k1, real parts only; out[256 n1 + j]
+        const int j = t;
+        constexpr R h = (R)0.86602540378443864676;
+        const V w1 = W[j], w2 = cmul(w1, w1);
+        const V y0 = buf[pad16(j)];
+        const V y1 = cmul(buf[pad16(j + 256)], cconj(w1));
+        const V y2 = cmul(buf[pad16(j + 512)], cconj(w2));
+        const R c = y0.x - (R)0.5 * (y1.x + y2.x), sn = h * (y1.y - y2.y);
+        const R r0 = y0.x + y1.x + y2.x, r1 = c - sn, r2 = c + sn;
+        auto put = [&](int o, R r) {
+            if (o < bins) {
+                const float f = (float)r;
+                eo[o] = f > 0.0f ? f : 0.0f;
+            }
+        };
+        put(j, r0);
+        put(j + 256, r1);
+        put(j + 512, r2);
+    }
+}
 } // namespace snb

@@ -429,24 +429,34 @@ __device__ __forceinline__ void fir_polyphase(const R* ph, const R* comp, const 
     }
 }
 
-template <typename R, int G, int M>
+// FF: the smoothing FIR by 768-point FFTs (fir_fft768; M == 4096 only)
+template <typename R, int G, int M, bool FF = false>
 __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 ? SNB_ENV_MINB : SNB_ENV_MINB_F32) / G)
     k_envelope(EnvArgs a, FirTaps<R> taps) {
+    static_assert(!FF || M == 4096, "FFT FIR: N = 8192 only");
     using V = typename Cx<R>::T;
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int N = 2 * M;
     const int grp = gidx(), tid = gtid();
     constexpr bool kSmemTw = M == kTwSharedM;
     V* tws = reinterpret_cast<V*>(smem);                   // compact twiddles (M == 4096)
-    R* comp = reinterpret_cast<R*>(tws + (kSmemTw ? kTwSharedCount : 0));
+    // FF: the FFT FIR's spectrum factors and twiddles, shared by the groups
+    V* ffu = tws + (kSmemTw ? kTwSharedCount : 0);
+    V* ffw = ffu + (FF ? kFfU : 0);
+    R* comp = reinterpret_cast<R*>(ffw + (FF ? kFfW : 0));
     // taps in shared memory: phase-major kFirTaps (fast path) or the reversed
-    // composite kernel (generic path)
-    const int comp_pad = a.fir_fast ? kFirTaps : (a.fir_q * a.decim + 1) & ~1;
-    const int group_reals = envelope_group_reals(N, a.decim * a.phase_len);
+    // composite kernel (generic path); none with the FFT FIR
+    const int comp_pad = FF ? 0 : a.fir_fast ? kFirTaps : (a.fir_q * a.decim + 1) & ~1;
+    const int group_reals = envelope_group_reals(N, FF ? 0 : a.decim * a.phase_len);
     V* bufB = reinterpret_cast<V*>(comp + comp_pad + (size_t)grp * group_reals);
     const R* cr = reinterpret_cast<const R*>(a.comp);
     const V* tw = reinterpret_cast<const V*>(a.tw);
-    if (a.fir_fast) {
+    if constexpr (FF) {
+        const V* su = reinterpret_cast<const V*>(a.ff_u);
+        const V* sw = reinterpret_cast<const V*>(a.ff_w);
+        for (int i = threadIdx.x; i < kFfU; i += blockDim.x) ffu[i] = su[i];
+        for (int i = threadIdx.x; i < kFfW; i += blockDim.x) ffw[i] = sw[i];
+    } else if (a.fir_fast) {
         for (int i = threadIdx.x; i < comp_pad; i += blockDim.x) comp[i] = taps.c[i]; // phase-major
     } else {
         for (int i = threadIdx.x; i < comp_pad; i += blockDim.x) comp[i] = i < a.comp_len ? cr[i] : (R)0;
@@ -517,6 +527,7 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
             const unsigned dmagic = 0xffffffffu / (unsigned)D + 1u; // exact for t < 2^32 / D
             const V* bsrc = reinterpret_cast<const V*>(src);
             const int Li = (int)L;
+            constexpr bool ffir = FF;
             auto sink = [&](int n, V h) {
                 const V bv = __ldg(bsrc + n);
                 const R m0 = fast_sqrt(bv.x * bv.x + h.x * h.x);
@@ -524,8 +535,14 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
                 const unsigned t = 2u * (unsigned)n + (unsigned)c0;
                 const int u = (int)__umulhi(t, dmagic);
                 const int pp = (int)t - u * D;
-                if (2 * n < Li) ph[pp * PL + u] = m0;
-                if (2 * n + 1 < Li) ph[pp + 1 == D ? u + 1 : (pp + 1) * PL + u] = m1;
+                if constexpr (ffir) {
+                    // fir_fft768's layout (D == 10, c0 odd: pp odd): both
+                    // samples in the complex slot u of sequence (pp - 1) / 2
+                    if (2 * n < Li) bufB[ff_slot((pp - 1) >> 1, u)] = V{m0, 2 * n + 1 < Li ? m1 : (R)0};
+                } else {
+                    if (2 * n < Li) ph[pp * PL + u] = m0;
+                    if (2 * n + 1 < Li) ph[pp + 1 == D ? u + 1 : (pp + 1) * PL + u] = m1;
+                }
             };
             if constexpr (M == 4096) {
                 dit_pass2_4096(bufB, twsrc);
@@ -535,7 +552,19 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
             }
             // zero the slots whose sample lies outside [0, L): per phase row p,
             // u < ceil((c0 - p) / D) and u >= ceil((L + c0 - p) / D)
-            if (tid < D) {
+            if constexpr (ffir) {
+                // slot (a, u) holds samples n = 10 u + 2 a + 1 - c0 and n + 1:
+                // zero for u < lo_a and u >= hi_a (at most 32 on either side,
+                // checked on the host)
+                for (int idx = tid; idx < 64 * kFfSeq; idx += kGroupThreads) {
+                    const int sa = idx >> 6, k = idx & 63;
+                    const int e = c0 - 1 - 2 * sa;
+                    const int lo = e > 0 ? (e + kFirD - 1) / kFirD : 0; // D == kFirD (host check)
+                    const int hi = (int)((L + e + kFirD - 1) / kFirD);
+                    const int u = k < 32 ? k : hi + (k - 32);
+                    if (k < 32 ? u < lo : u < kFfL) bufB[ff_slot(sa, u)] = V{(R)0, (R)0};
+                }
+            } else if (tid < D) {
                 const int p = tid;
                 const int lo = c0 >= p ? (c0 - p + D - 1) / D : 0;
                 const int hi = (int)((L + c0 - p + D - 1) / D);
@@ -544,13 +573,24 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
                 for (int k = hi; k < a.phase_len; ++k) row[k] = 0;
             }
         }
+        const int64_t nx = it + (int64_t)gridDim.x * G;
         if constexpr (M == 4096) {
-            const int64_t nx = it + (int64_t)gridDim.x * G;
-            if (nx < items) load_pre(nx);
+            if (!FF && nx < items) load_pre(nx);
         }
         gsync();
         float* eo = a.energy + ((size_t)b * a.n_dirs + a.order[slot]) * a.bins;
-        fir_polyphase<R>(ph, comp, a, eo);
+        if constexpr (M == 4096) {
+            if constexpr (FF) {
+                // (the next item's early first-pass loads come after the FFT FIR:
+                // its radix-16 passes need the whole register budget)
+                fir_fft768(bufB, ffu, ffw, eo, (int)a.bins);
+                if (nx < items) load_pre(nx);
+            } else {
+                fir_polyphase<R>(ph, comp, a, eo);
+            }
+        } else {
+            fir_polyphase<R>(ph, comp, a, eo);
+        }
         gsync();
     }
 }
@@ -801,8 +841,40 @@ static void env_launch(const EnvArgs& a, const FirTaps<R>& taps, int grid, size_
     k_envelope<R, G, M><<<grid, kThreads * G, smem, s>>>(a, taps);
 }
 
+// FFT FIR variant (N = 8192): kFfGroups groups per CTA share the spectrum
+// factors and twiddles in shared memory
+size_t envelope_ff_smem_bytes(bool f32) {
+    const size_t rb = f32 ? 4 : 8;
+    return ((size_t)kTwSharedCount + kFfU + kFfW) * 2 * rb + (size_t)kFfGroups * envelope_group_reals(8192, 0) * rb;
+}
+
+int envelope_ff_blocks_per_sm(bool f32) {
+    int n = 1;
+    const size_t smem = envelope_ff_smem_bytes(f32);
+    if (f32) {
+        set_smem((const void*)k_envelope<float, kFfGroups, 4096, true>, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_envelope<float, kFfGroups, 4096, true>, kThreads * kFfGroups, smem);
+    } else {
+        set_smem((const void*)k_envelope<double, kFfGroups, 4096, true>, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_envelope<double, kFfGroups, 4096, true>, kThreads * kFfGroups, smem);
+    }
+    return n > 0 ? n : 0;
+}
+
+template <typename R>
+static void env_ff_launch(const EnvArgs& a, const FirTaps<R>& taps, int grid, cudaStream_t s) {
+    const size_t smem = envelope_ff_smem_bytes(sizeof(R) == 4);
+    set_smem((const void*)k_envelope<R, kFfGroups, 4096, true>, smem);
+    k_envelope<R, kFfGroups, 4096, true><<<grid, kThreads * kFfGroups, smem, s>>>(a, taps);
+}
+
 void launch_envelope(const EnvArgs& a, const FirTaps<float>& t32, const FirTaps<double>& t64, bool f32,
                      int grid, cudaStream_t s) {
+    if (a.fir_fft) {
+        if (f32) env_ff_launch<float>(a, t32, grid, s);
+        else env_ff_launch<double>(a, t64, grid, s);
+        return;
+    }
     if (f32) {
         const size_t smem = envelope_smem_bytes(a.n, a.fir_q * a.decim, a.decim * a.phase_len, true, kEnvGroupsF32);
         SNB_DISPATCH_M(a.n / 2, (env_launch<float, kEnvGroupsF32, MM>(a, t32, grid, smem, s)))

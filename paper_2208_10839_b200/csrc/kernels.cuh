@@ -75,6 +75,9 @@ struct EnvArgs {
     int fir_q;               // ceil(comp_len / decim): taps per phase
     int phase_len;           // entries per phase row (>= bins + fir_q + FIR_R)
     int fir_fast;            // decim == kFirD, fir_q == kFirQ, bins <= 128 * kFirR
+    int fir_fft;             // FIR by 768-point FFTs (fir_fft768, fft.cuh): N == 8192 and the shapes fit
+    const void* ff_u;        // [16][240] spectrum factors U_a in register order (double2 or float2)
+    const void* ff_w;        // e^{-2 pi i e / 768}, e < 768
 };
 
 // Polyphase smoothing FIR fast path (the reference's default composite
@@ -101,6 +104,9 @@ void launch_beamform_tiles(const BeamArgs& a, bool f32, cudaStream_t s);
 void launch_envelope(const EnvArgs& a, const FirTaps<float>& t32, const FirTaps<double>& t64, bool f32,
                      int grid, cudaStream_t s);
 size_t envelope_smem_bytes(int n, int comp_taps_padded, int phase_reals, bool f32, int groups);
+constexpr int kFfGroups = 2;        // FFT FIR envelope: groups per CTA (shared factor tables)
+size_t envelope_ff_smem_bytes(bool f32);
+int envelope_ff_blocks_per_sm(bool f32); // 0: does not fit
 __host__ __device__ int envelope_group_reals(int n, int phase_reals);
 int envelope_blocks_per_sm(bool f32, int n_fft, size_t smem);
 void launch_rfft_forward(const double* x, double2* X, const double2* tw, int n, size_t smem,

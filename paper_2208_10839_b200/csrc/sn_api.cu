@@ -160,6 +160,12 @@ struct sn_workspace {
     float2* d_tw_env32 = nullptr;
     double2* d_tw_small = nullptr;
     float2* d_tw_small32 = nullptr;
+    // FIR by FFT (fir_fft768): spectrum factors and 768-point twiddles
+    int fir_fft = 0;
+    double2* d_ff_u = nullptr;
+    float2* d_ff_u32 = nullptr;
+    double2* d_ff_w = nullptr;
+    float2* d_ff_w32 = nullptr;
     uint8_t* h_in = nullptr;
     float* h_out = nullptr;
     // launch shapes
@@ -230,7 +236,7 @@ struct sn_workspace {
         for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
                         (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot,  (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
-                        (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32, (void*)d_tw_small, (void*)d_tw_small32, (void*)d_planes, (void*)d_dwords, (void*)d_resid,
+                        (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32, (void*)d_tw_small, (void*)d_tw_small32, (void*)d_ff_u, (void*)d_ff_u32, (void*)d_ff_w, (void*)d_ff_w32, (void*)d_planes, (void*)d_dwords, (void*)d_resid,
                         (void*)d_tc_R, (void*)d_tc_base, (void*)d_amax, (void*)d_tc_start, (void*)d_tc_size,
                         (void*)d_crc_slice, (void*)d_crc_shift, (void*)d_crc_lane, (void*)d_img_tpl, (void*)d_frames_out,
                         (void*)d_frames_in, (void*)d_ids, (void*)d_crc_acc, (void*)d_crc_ok}) {
@@ -410,6 +416,7 @@ struct sn_workspace {
             phase_len = std::max(phase_len, (int)s.bins + fir_q + 1);
             phase_len = (phase_len + 1) & ~1; // even: rows stay 16-byte aligned (paired loads)
             fir_fast = D == kFirD && fir_q == kFirQ && groups <= 128;
+            init_fir_fft(D, c0);
             if (fir_fast) {
                 for (int p = 0; p < kFirD; ++p) {
                     for (int q = 0; q < kFirQ; ++q) {
@@ -426,6 +433,11 @@ struct sn_workspace {
                                        f32 ? kEnvGroupsF32 : kEnvGroupsF64);
         {
             dir_grid = sms * envelope_blocks_per_sm(f32, (int)s.env_fft, dir_smem);
+            if (fir_fft) {
+                const int per = envelope_ff_blocks_per_sm(f32);
+                if (per > 0) dir_grid = sms * per;
+                else fir_fft = 0; // does not fit: direct polyphase FIR
+            }
         }
         mf_smem = fft_smem_bytes((int)s.mf_fft, sizeof(double));
         init_frames();
@@ -705,7 +717,98 @@ struct sn_workspace {
         ea.fir_q = fir_q;
         ea.phase_len = phase_len;
         ea.fir_fast = fir_fast;
+        ea.fir_fft = fir_fft;
+        ea.ff_u = f32 ? (const void*)d_ff_u32 : (const void*)d_ff_u;
+        ea.ff_w = f32 ? (const void*)d_ff_w32 : (const void*)d_ff_w;
         launch_envelope(ea, taps32, taps64, f32, dir_grid, s);
+    }
+
+    // FIR by 768-point FFTs (fir_fft768 in fft.cuh) for the default shapes:
+    // N = 8192, decimation 10, 45 taps per phase, bins + 44 <= 768 and at most
+    // 32 zero slots per phase on either side of the envelope. Host tables: the
+    // spectrum factors U_a[k] = (conj Ghat_re[k] - i conj Ghat_im[k]) / 768 (re/im
+    // phases of sequence a as laid out by the sink, fft.cuh),
+    // Ghat_p = DFT768 of the phase taps G_p[q] = rev[10 q + p] (long double),
+    // stored in the register order of the third forward pass, and the
+    // twiddles w768^j (j < 256) and w256^{n3 k2} (16 x 16). SNB_FIR_DIRECT (build macro, A/B) keeps
+    // the direct polyphase FIR.
+    void init_fir_fft(int D, int c0) {
+        const Sizes& s = plan.sz;
+        fir_fft = 0;
+#ifndef SNB_FIR_DIRECT
+        if (s.env_fft != 8192 || D != kFirD || fir_q != kFirQ || c0 % 2 != 1 || s.bins + kFirQ - 1 > (uint64_t)kFfL)
+            return;
+        for (int sa = 0; sa < kFfSeq; ++sa) {
+            // slot (sa, u) holds samples 10 u + 2 sa + 1 - c0 and the next one
+            const int64_t e = c0 - 1 - 2 * sa;
+            const int64_t lo = e > 0 ? (e + D - 1) / D : 0;
+            const int64_t hi = ((int64_t)s.mf_len + e + D - 1) / D;
+            // hi < 768: the last slot of sequence 4 (E_0 advanced by one, read
+            // cyclically at index -1) must be a zero
+            if (lo > 32 || hi >= kFfL || kFfL - hi > 32) return;
+        }
+        const long double pi2 = 6.283185307179586476925286766559L;
+        std::vector<long double> gr(D * kFfL), gi(D * kFfL); // conj Ghat_p[k]
+        for (int p = 0; p < D; ++p) {
+            for (int k = 0; k < kFfL; ++k) {
+                long double re = 0, im = 0;
+                for (int q = 0; q < kFirQ; ++q) {
+                    const size_t j = (size_t)q * D + p;
+                    if (j >= plan.comp_rev.size()) continue;
+                    const long double g = plan.comp_rev[j];
+                    const long double ang = pi2 * (long double)((k * q) % kFfL) / kFfL;
+                    re += g * cosl(ang);
+                    im += g * sinl(ang); // conj: e^{+2 pi i k q / 768}
+                }
+                gr[p * kFfL + k] = re;
+                gi[p * kFfL + k] = im;
+            }
+        }
+        // sequence a: real part phase 2a + 1, imaginary part phase 2a + 2
+        // (a < 4) or phase 0 advanced by one sample (a = 4: conj Ghat_0 times
+        // e^{-2 pi i k / 768}, its taps delayed by one cyclically)
+        std::vector<double2> u(kFfU);
+        for (int t = 0; t < kFfThreads; ++t) {
+            const int a = t / 48, k1 = (t % 48) / 16, k2 = t % 16;
+            for (int r = 0; r < 16; ++r) {
+                const int k3 = (r >> 2) + 4 * (r & 3); // out_slot<16>(r)
+                const int k = k1 + 3 * k2 + 48 * k3;
+                const size_t pr = (size_t)(2 * a + 1) * kFfL + k, pi = (size_t)((2 * a + 2) % D) * kFfL + k;
+                long double ir = gr[pi], ii = gi[pi];
+                if (a == kFfSeq - 1) {
+                    const long double ang = pi2 * k / kFfL, c = cosl(ang), sn = -sinl(ang);
+                    const long double xr = ir * c - ii * sn, xi = ir * sn + ii * c;
+                    ir = xr;
+                    ii = xi;
+                }
+                // (conj Ghat_re - i conj Ghat_im) / 768
+                u[(size_t)r * kFfThreads + t] = double2{(double)((gr[pr] + ii) / kFfL), (double)((gi[pr] - ir) / kFfL)};
+            }
+        }
+        std::vector<double2> w(kFfW); // w768^j (j < 256); w256^{n3 k2} at 256 + 16 k2 + n3
+        for (int e = 0; e < 256; ++e) {
+            const long double a1 = pi2 * e / kFfL, a2 = pi2 * ((e >> 4) * (e & 15)) / 256;
+            w[e] = double2{(double)cosl(a1), (double)-sinl(a1)};
+            w[256 + e] = double2{(double)cosl(a2), (double)-sinl(a2)};
+        }
+        uint64_t& n = device_allocs;
+        d_ff_u = dmalloc<double2>(u.size(), n);
+        d_ff_w = dmalloc<double2>(w.size(), n);
+        d_ff_u32 = dmalloc<float2>(u.size(), n);
+        d_ff_w32 = dmalloc<float2>(w.size(), n);
+        upload(d_ff_u, u, stream);
+        upload(d_ff_w, w, stream);
+        std::vector<float2> u32(u.size()), w32(w.size());
+        for (size_t i = 0; i < u.size(); ++i) u32[i] = float2{(float)u[i].x, (float)u[i].y};
+        for (size_t i = 0; i < w.size(); ++i) w32[i] = float2{(float)w[i].x, (float)w[i].y};
+        upload(d_ff_u32, u32, stream);
+        upload(d_ff_w32, w32, stream);
+        fir_fft = 1;
+#else
+        (void)s;
+        (void)D;
+        (void)c0;
+#endif
     }
 
     void validate(const sn_raw_measurement& m) const { // pipeline.cpp:524-540
