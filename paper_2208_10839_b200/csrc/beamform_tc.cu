@@ -340,11 +340,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
                 build_A(c);
                 cur_c = c;
             }
+#ifdef SNB_TC_EARLY_RELOAD
             // window g + kWin - 1 reuses the buffer of tile g - 1
             if (g + kWin - 1 < ntile) {
                 if (g >= 1) mbar_wait(&wfree[(g - 1) % kWin], (uint32_t)(((g - 1) / kWin) & 1));
                 load_window(g + kWin - 1);
             }
+#endif
             mbar_wait(&wfull[g % kWin], (uint32_t)((g / kWin) & 1));
             const uint32_t bbase = bw_addr + (uint32_t)((g % kWin) * bbuf);
             const uint64_t a0 = sdesc(ares_addr, kTcM * 16, 128);
@@ -371,6 +373,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
             }
             if (leader) mma_commit(&wfree[g % kWin]);
             __syncwarp();
+#ifndef SNB_TC_EARLY_RELOAD
+            // window g + kWin - 1 reuses the buffer of tile g - 1: wait for the
+            // MMAs of tile g - 1 only after tile g's are queued behind them, so
+            // the tensor pipe never drains at a tile boundary
+            if (g + kWin - 1 < ntile) {
+                if (g >= 1) mbar_wait(&wfree[(g - 1) % kWin], (uint32_t)(((g - 1) / kWin) & 1));
+                load_window(g + kWin - 1);
+            }
+#endif
         }
     } else {
         // ======================== epilogue warps 0-15 =========================

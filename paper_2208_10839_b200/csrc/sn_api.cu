@@ -596,18 +596,29 @@ struct sn_workspace {
         tc_grid = std::min(sms, kTcMaxGrid);
     }
 
-    // contiguous per-CTA tile ranges of equal estimated work (R_c + 8 units
-    // per tile: MMAs plus window load and epilogue)
+    // contiguous per-CTA tile ranges of equal estimated work. A tile costs
+    // the larger of its MMA time (R_c units of six MMAs) and the epilogue's
+    // drain + recombination of six accumulators (independent of R_c,
+    // kTcEpiUnits of the same units), plus a small fixed part
+#ifndef SNB_TC_EPI_UNITS
+#define SNB_TC_EPI_UNITS 20 // A/B on hemisphere3000 (beamform ms): 8: 1.347, 14: 1.390, 16: 1.322, 20: 1.287, 24: 1.287
+#endif
+#ifndef SNB_TC_FIXED_UNITS
+#define SNB_TC_FIXED_UNITS 2
+#endif
+    static double tc_tile_cost(int R) {
+        return std::max<double>(R, SNB_TC_EPI_UNITS) + SNB_TC_FIXED_UNITS;
+    }
     TcSched tc_schedule(int count) const {
         TcSched sc{};
         const int per_c = count * tc_ntiles;
         double total = 0;
-        for (int c = 0; c < tc_clusters; ++c) total += (double)(tc_R[c] + 8) * per_c;
+        for (int c = 0; c < tc_clusters; ++c) total += tc_tile_cost(tc_R[c]) * per_c;
         int k = 1;
         double acc = 0;
         sc.start[0] = 0;
         for (int c = 0; c < tc_clusters && k < tc_grid; ++c) {
-            const double w = tc_R[c] + 8;
+            const double w = tc_tile_cost(tc_R[c]);
             while (k < tc_grid && acc + w * per_c >= total * k / tc_grid) {
                 const double need = total * k / tc_grid - acc;
                 int m = (int)std::ceil(need / w);
@@ -1163,6 +1174,9 @@ sn_status sn_workspace_create(const sn_pipeline_config* cfg, int device, uint64_
         ws->plan_tensor_core_beamformer();
         if (cfg->precision != SN_PRECISION_F64 && cfg->precision != SN_PRECISION_F32) {
             config_error("pipeline: unknown precision mode");
+        }
+        if (ws->max_batch * ws->plan.sz.n_dirs >= (uint64_t{1} << 31)) {
+            argument_error("max_batch x directions must stay below 2^31 (per-launch work items)");
         }
         if (device >= 0) ws->init_device();
         *out = ws.release();
