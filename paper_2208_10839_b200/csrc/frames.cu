@@ -21,6 +21,7 @@
 #include "kernels.cuh"
 
 #include <cstdint>
+#include <cstring>
 
 namespace snb {
 
@@ -256,28 +257,42 @@ void launch_crc_finalize(uint32_t* acc, uint32_t k_n, uint64_t count, uint8_t* o
 }
 
 // ---- host side: tables and the constant of the init term --------------------
-static uint32_t host_tab[256];
-
-static void host_tables_init() {
-    static bool done = false;
-    if (done) return;
-    for (uint32_t i = 0; i < 256; ++i) {
-        uint32_t c = i;
-        for (int k = 0; k < 8; ++k) c = (c & 1) ? (0xEDB88320u ^ (c >> 1)) : (c >> 1);
-        host_tab[i] = c;
+// slicing-by-8 tables, built once (C++11 magic static: thread-safe first use)
+struct HostCrcTables {
+    uint32_t t[8][256];
+    HostCrcTables() {
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; ++k) c = (c & 1) ? (0xEDB88320u ^ (c >> 1)) : (c >> 1);
+            t[0][i] = c;
+        }
+        for (int s = 1; s < 8; ++s)
+            for (int i = 0; i < 256; ++i) t[s][i] = t[0][t[s - 1][i] & 0xFF] ^ (t[s - 1][i] >> 8);
     }
-    done = true;
+};
+static const HostCrcTables& host_crc() {
+    static const HostCrcTables tabs;
+    return tabs;
 }
 
 uint32_t crc32_host(const uint8_t* p, uint64_t n) {
-    host_tables_init();
+    const HostCrcTables& T = host_crc();
     uint32_t c = 0xFFFFFFFFu;
-    for (uint64_t i = 0; i < n; ++i) c = host_tab[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+    uint64_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        uint32_t lo, hi;
+        std::memcpy(&lo, p + i, 4);
+        std::memcpy(&hi, p + i + 4, 4);
+        lo ^= c;
+        c = T.t[7][lo & 0xFF] ^ T.t[6][(lo >> 8) & 0xFF] ^ T.t[5][(lo >> 16) & 0xFF] ^ T.t[4][lo >> 24] ^
+            T.t[3][hi & 0xFF] ^ T.t[2][(hi >> 8) & 0xFF] ^ T.t[1][(hi >> 16) & 0xFF] ^ T.t[0][hi >> 24];
+    }
+    for (; i < n; ++i) c = T.t[0][(c ^ p[i]) & 0xFF] ^ (c >> 8);
     return c ^ 0xFFFFFFFFu;
 }
 
 void crc_tables_host(uint32_t* slice /* 1024 */, uint32_t* shift /* kCrcShiftMats x 32 */) {
-    host_tables_init();
+    const uint32_t* host_tab = host_crc().t[0];
     for (int i = 0; i < 256; ++i) {
         uint32_t c = host_tab[i];
         slice[i] = c;

@@ -126,10 +126,20 @@ struct sn_pool {
             for (auto it = pending.begin(); it != pending.end();) {
                 auto& nr = next_release[it->first.first];
                 if (nr == it->first.second) {
+                    const uint32_t serial = it->first.first;
                     ++nr;
                     released.push_back(std::move(it->second));
                     it = pending.erase(it);
                     moved = true;
+                    // a sensor with nothing queued, in flight or pending drops
+                    // its counters (the ticket is assigned before the CRC is
+                    // verified, so a corrupted serial would otherwise leave a
+                    // map entry behind for good); its next frame restarts at 0
+                    auto nt = next_ticket.find(serial);
+                    if (nt != next_ticket.end() && nt->second == nr) {
+                        next_ticket.erase(nt);
+                        next_release.erase(serial);
+                    }
                 } else {
                     ++it;
                 }

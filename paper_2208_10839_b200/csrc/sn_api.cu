@@ -121,6 +121,13 @@ struct sn_workspace {
     // s_env2 so that a chunk's CTAs fill the SMs its predecessor's tail frees
     cudaStream_t s_env2 = nullptr;
     cudaEvent_t ev_beams = nullptr;
+    // completion of the most recent call's device work, whatever stream it
+    // ran on: every entry point orders its first device operation after it
+    // (a device call on a caller stream followed by a host call, or two
+    // device calls on different streams, share the scratch buffers)
+    cudaEvent_t ev_last = nullptr;
+    void after_last(cudaStream_t s) const { ck(cudaStreamWaitEvent(s, ev_last, 0), "wait last"); }
+    void mark_last(cudaStream_t s) const { ck(cudaEventRecord(ev_last, s), "record last"); }
     static constexpr int kMaxChunks = 16;
     // envelope chunk sizes of a block of c captures: ~2 per chunk, the last
     // chunk a single capture (its download is the exposed one)
@@ -206,7 +213,18 @@ struct sn_workspace {
     FirTaps<double> taps64{};
     FirTaps<float> taps32{};
     uint64_t packed_bytes = 0, energy_per = 0, lp = 0;
+    // device_allocs: buffers allocated while the workspace is built;
+    // alloc_events (Workspace::allocation_events, pipeline.cpp:343-348): every
+    // allocation after construction, all of which go through runtime_alloc
     uint64_t alloc_events = 0, device_allocs = 0, last_launches = 0;
+    template <typename T>
+    T* runtime_alloc(size_t n) {
+        ++alloc_events;
+        return dmalloc<T>(n, device_allocs);
+    }
+    // scratch of the beamform() accessor, allocated on its first call
+    double* d_bf_in = nullptr;
+    double* d_bf_out = nullptr;
     // optional per-stage timing (events on the launching stream)
     bool profiling = false;
     cudaEvent_t ev[6] = {};
@@ -233,13 +251,14 @@ struct sn_workspace {
         if (s_d2h) cudaStreamDestroy(s_d2h);
         if (s_env2) cudaStreamDestroy(s_env2);
         if (ev_beams) cudaEventDestroy(ev_beams);
+        if (ev_last) cudaEventDestroy(ev_last);
         for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
                         (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot,  (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
                         (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32, (void*)d_tw_small, (void*)d_tw_small32, (void*)d_ff_u, (void*)d_ff_u32, (void*)d_ff_w, (void*)d_ff_w32, (void*)d_planes, (void*)d_dwords, (void*)d_resid,
                         (void*)d_tc_R, (void*)d_tc_base, (void*)d_amax, (void*)d_tc_start, (void*)d_tc_size,
                         (void*)d_crc_slice, (void*)d_crc_shift, (void*)d_crc_lane, (void*)d_img_tpl, (void*)d_frames_out,
-                        (void*)d_frames_in, (void*)d_ids, (void*)d_crc_acc, (void*)d_crc_ok}) {
+                        (void*)d_frames_in, (void*)d_ids, (void*)d_crc_acc, (void*)d_crc_ok, (void*)d_bf_in, (void*)d_bf_out}) {
             if (p) cudaFree(p);
         }
         if (h_in) cudaFreeHost(h_in);
@@ -268,6 +287,7 @@ struct sn_workspace {
         ck(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&s_env2, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaEventCreateWithFlags(&ev_beams, cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&ev_last, cudaEventDisableTiming), "cudaEventCreate");
         for (int j = 0; j < kMaxChunks; ++j) {
             ck(cudaEventCreateWithFlags(&ev_in[j], cudaEventDisableTiming), "cudaEventCreate");
             ck(cudaEventCreateWithFlags(&ev_done[j], cudaEventDisableTiming), "cudaEventCreate");
@@ -863,6 +883,8 @@ struct sn_workspace {
         require_device();
         DeviceGuard g(device);
         const bool out_pinned = is_pinned(out);
+        after_last(s_h2d);
+        after_last(stream);
         uint64_t done = 0;
         while (done < count) {
             const uint64_t c = std::min(max_batch, count - done);
@@ -913,6 +935,7 @@ struct sn_workspace {
             if (!out_pinned) std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
             done += c;
         }
+        mark_last(s_d2h);
     }
 
     // wire::error_frame(serial, ts, seq, message) (wire.cpp:278-287)
@@ -943,6 +966,7 @@ struct sn_workspace {
         DeviceGuard g(device);
         const Sizes& z = plan.sz;
         const bool out_pinned = is_pinned(out);
+        after_last(stream);
         std::vector<uint64_t> batch;
         batch.reserve(max_batch);
         auto flush = [&]() {
@@ -1061,6 +1085,16 @@ struct sn_workspace {
             try {
                 validate(m);
             } catch (const Error& e) {
+                // the nominal-size frames skipped the host CRC above (it runs on
+                // the GPU with the batch); a rejected one is checked here first,
+                // so a corrupted header is discarded as an integrity error
+                // (wire.cpp:136-145) instead of answered with an error frame
+                // carrying corrupted ids
+                if (len == in_frame_len) {
+                    uint32_t stored;
+                    std::memcpy(&stored, f + 36 + plen, 4);
+                    if (stored != crc32_host(f, 36 + plen)) continue;
+                }
                 const auto ef = error_frame(m.sensor_serial, m.timestamp_us, m.seq, e.what());
                 if (ef.size() <= slot) {
                     std::memcpy(out + k * slot, ef.data(), ef.size());
@@ -1073,6 +1107,7 @@ struct sn_workspace {
             if (batch.size() == max_batch) flush();
         }
         flush();
+        mark_last(stream);
         (void)z;
     }
 
@@ -1080,12 +1115,14 @@ struct sn_workspace {
         require_device();
         DeviceGuard g(device);
         if (!s) s = stream;
+        after_last(s);
         uint64_t done = 0;
         while (done < count) {
             const uint64_t c = std::min(max_batch, count - done);
             enqueue(d_in + done * packed_bytes, c, d_out + done * energy_per, s);
             done += c;
         }
+        mark_last(s);
     }
 };
 
@@ -1231,6 +1268,8 @@ sn_status sn_workspace_process_device_graph(sn_workspace* ws, const uint8_t* d_p
                 cudaGraphExecDestroy(ws->graph);
                 ws->graph = nullptr;
             }
+            ws->after_last(ws->stream);
+            ck(cudaStreamSynchronize(ws->stream), "sync before capture");
             cudaGraph_t graph;
             ck(cudaStreamBeginCapture(ws->stream, cudaStreamCaptureModeThreadLocal), "capture");
             ws->enqueue(d_packed, count, d_energies, ws->stream);
@@ -1241,7 +1280,9 @@ sn_status sn_workspace_process_device_graph(sn_workspace* ws, const uint8_t* d_p
             ws->g_out = d_energies;
             ws->g_count = count;
         }
+        ws->after_last(s);
         ck(cudaGraphLaunch(ws->graph, s), "graph launch");
+        ws->mark_last(s);
         ws->last_launches = ws->tc ? 7 : 5;
     });
 }
@@ -1302,7 +1343,7 @@ sn_status sn_workspace_stage(sn_workspace* ws, int32_t stage, uint64_t item, dou
         }
         if (capacity < n) argument_error("buffer too small");
         DeviceGuard g(ws->device);
-        ck(cudaStreamSynchronize(ws->stream), "sync");
+        ck(cudaEventSynchronize(ws->ev_last), "sync");
         if (stage == SN_STAGE_FILT || stage == SN_STAGE_PREMF) {
             const uint64_t pitch = stage == SN_STAGE_FILT ? ws->lp : z.mf_fft;
             ck(cudaMemcpy2D(out, z.mf_len * sizeof(double), src, pitch * sizeof(double),
@@ -1329,19 +1370,17 @@ sn_status sn_workspace_beamform(sn_workspace* ws, const double* filtered, uint64
         ws->require_device();
         DeviceGuard g(ws->device);
         const uint64_t L = z.mf_len;
-        double *d_in = nullptr, *d_out = nullptr;
-        ck(cudaMalloc(&d_in, kCh * L * sizeof(double)), "cudaMalloc");
-        ck(cudaMalloc(&d_out, z.n_dirs * L * sizeof(double)), "cudaMalloc");
-        cudaError_t e = cudaMemcpyAsync(d_in, filtered, kCh * L * sizeof(double), cudaMemcpyHostToDevice, ws->stream);
-        if (e == cudaSuccess) {
-            launch_beamform(d_in, d_out, ws->d_shifts, (int64_t)L, (int64_t)z.n_dirs, ws->stream);
-            e = cudaGetLastError();
-        }
-        if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_out, z.n_dirs * L * sizeof(double), cudaMemcpyDeviceToHost, ws->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(ws->stream);
-        cudaFree(d_in);
-        cudaFree(d_out);
-        ck(e, "beamform");
+        // the accessor is off the hot path: its two scratch buffers are
+        // allocated on the first call (counted in allocation_events) and reused
+        if (!ws->d_bf_in) ws->d_bf_in = ws->runtime_alloc<double>(kCh * L);
+        if (!ws->d_bf_out) ws->d_bf_out = ws->runtime_alloc<double>(z.n_dirs * L);
+        ws->after_last(ws->stream);
+        ck(cudaMemcpyAsync(ws->d_bf_in, filtered, kCh * L * sizeof(double), cudaMemcpyHostToDevice, ws->stream), "H2D");
+        launch_beamform(ws->d_bf_in, ws->d_bf_out, ws->d_shifts, (int64_t)L, (int64_t)z.n_dirs, ws->stream);
+        ck(cudaGetLastError(), "beamform launch");
+        ck(cudaMemcpyAsync(out, ws->d_bf_out, z.n_dirs * L * sizeof(double), cudaMemcpyDeviceToHost, ws->stream), "D2H");
+        ws->mark_last(ws->stream);
+        ck(cudaStreamSynchronize(ws->stream), "beamform");
     });
 }
 
