@@ -48,6 +48,11 @@ GRIDS = {"horizontal90": 0, "box1850": 1, "hemisphere3000": 2, "az181": 3}
 # tcgen05 kind::i8 on this pool (the M=128, N=64 shape the beamformer issues
 # is capped at ~2.9-3.0 POPS by the ~50-cycle per-instruction floor)
 TC_INT8_PEAK = 4500.0
+# the reference links FFTW3 (core/CMakeLists.txt:3), which this image lacks:
+# the CPU reference runs with a test-only radix-2 FFTW-API stand-in
+# (oracle/fftw_shim), slower than FFTW on the FFT-bound stages, so GPU/CPU
+# ratios overstate the gap to a real-FFTW build by an unknown factor
+FFT_LABEL = "radix2-shim (oracle/fftw_shim; FFTW3 absent from the image)"
 
 
 def parse_args():
@@ -64,8 +69,16 @@ def parse_args():
     p.add_argument("--latency-samples", type=int, default=50)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-calls", type=int, default=2, help="reference calls per host thread")
-    p.add_argument("--stream-frames", type=int, default=512,
-                   help="frames of the 8-sensor streaming sample through the worker pool (0: skip)")
+    p.add_argument("--stream-frames", type=int, default=2048,
+                   help="frames of the 8-sensor streaming run through the worker pool (configs[3]: 256 "
+                        "measurements x 8 sensors; 0: skip)")
+    p.add_argument("--paced-frames", type=int, default=256,
+                   help="frames of the paced (10 Hz per sensor) latency sample")
+    p.add_argument("--cpu-latency-calls", type=int, default=20,
+                   help="timed reference process() calls per latency leg (bench.cpp:63-108 uses 100)")
+    p.add_argument("--no-sweep", action="store_true", help="skip the configs[4] grid x window sweep")
+    p.add_argument("--sweep-steps", type=int, default=3)
+    p.add_argument("--lib", default=None, help="developer A/B: another build of libsonarnet_b200.so")
     return p.parse_args()
 
 
@@ -201,10 +214,36 @@ def cpu_baseline(cfg_b200, grid, calls, warmup=1):
     elapsed, total = ref.throughput(rc, pool, threads, calls)
     return {
         "value": total / elapsed, "unit": UNIT, "cores": threads, "kind": "reference",
+        "fft": FFT_LABEL,
         "sample": (f"{total} process() calls of {grid} ({threads} threads x {calls}; "
                    f"unmodified reference core built -O3 -march=x86-64-v3, FFT = test-only "
                    f"FFTW-API shim; {elapsed:.2f} s wall)"),
     }
+
+
+def cpu_latency(grid, n):
+    """Reference single-measurement latency, the protocol of
+    bench::run_benchmark (bench.cpp:63-108): one Workspace with
+    processing_threads = 2 (the default, pipeline.hpp:33-36) and = nproc,
+    1 warm-up + n timed process() calls (steady_clock)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    ref = po.Ref(fast=True)
+    kind = 0 if grid == "az181" else GRIDS[grid]
+    rc = ref.default_config(kind)
+    if grid == "az181":
+        rc = rc.copy(directions=po.az181_directions(), grid_kind=3)
+    pk = ref.synthesize(rc, BENCH_SCENE, 0.01, 7)
+    out = {"protocol": f"bench.cpp:63-108: 1 warm-up + {n} timed process() calls per leg",
+           "fft": FFT_LABEL, "unit": "ms"}
+    nproc = os.cpu_count() or 1
+    for name, th in (("threads_2", 2), ("threads_nproc", nproc)):
+        ws = ref.workspace(rc.copy(processing_threads=th))
+        d = ws.latency(pk, n)
+        out[name] = {"threads": th, "n": n, "p50": float(np.percentile(d, 50)),
+                     "p99": float(np.percentile(d, 99)), "mean": float(np.mean(d)), "min": float(np.min(d))}
+        del ws
+    return out
 
 
 def run_reference(args):
@@ -229,7 +268,7 @@ def run_reference(args):
         "config": {"workload": f"1 eRTIS sensor, 32 mics, {args.grid}, 5 m window = 144800 PDM "
                                f"frames/capture; reference CPU path, {threads} workers x 1 thread",
                    "grid": args.grid},
-        "impl": "reference", "cpu_baseline": base,
+        "impl": "reference", "cpu_baseline": base, "fft": FFT_LABEL,
         "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -238,12 +277,91 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+SWEEP_GRIDS = ("horizontal90", "az181", "box1850", "hemisphere3000", "fib10k", "fib30k")
+SWEEP_RANGES = (1.5, 5.0, 10.0)
+
+
+def sweep_config(sn, grid, max_range, precision):
+    """configs[4] points: the built-in grids, az181, and Fibonacci hemispheres
+    of 10k / 30k directions (geometry.cpp:206-229 with n free), at a window
+    of max_range metres (frames / FFT sizes / bins per pipeline.cpp:40-52)."""
+    if grid.startswith("fib"):
+        n = int(grid[3:-1]) * 1000
+        cfg = sn.default_pipeline_config(sn.GridKind.horizontal90).copy(
+            directions=sn.fibonacci_hemisphere(n), grid_kind=3)
+        cfg = cfg.copy(precision=0 if precision == "f64" else 1)
+    else:
+        cfg = make_config(sn, grid, precision)
+    return cfg.copy(max_range=max_range)
+
+
+def sweep(sn, args, local, peak):
+    """BASELINE configs[4]: direction grid x recording length on this GPU
+    (N=1; one sensor per GPU at N>1 is the same per-GPU work, scaling weak).
+    Per point: B captures per step (B = 16 scaled down so a step's beams stay
+    near the default's), GPU-synthesised inputs, 1 warm-up + K timed steps on
+    the device path (CUDA events), then one profiled step for the stage
+    shares; `frac` = the envelope stage's algorithmic FLOPs
+    / its time / the live FP64 (or FP32) FMA peak."""
+    import torch
+    pts = []
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    for grid in SWEEP_GRIDS:
+        for mr in SWEEP_RANGES:
+            cfg = sweep_config(sn, grid, mr, args.precision)
+            d = cfg.dims()
+            n, N = d["n_directions"], d["env_fft_size"]
+            B = int(max(1, min(16, round(16 * 3000 * 8192 / (n * N)))))
+            t0 = time.perf_counter()
+            ws = sn.Workspace(cfg, device=local, max_batch=B)
+            setup_s = time.perf_counter() - t0
+            scenes = [sn.Scene([sn.Reflector(*r) for r in BENCH_SCENE[:1 if mr < 2 else 2]], 0.01, 7 + k)
+                      for k in range(2 * B)]
+            pin = torch.empty(2 * B * ws.packed_bytes, dtype=torch.uint8, device=dev)
+            sn.synthesize_device(cfg, scenes, pin.data_ptr(), device=local)
+            out = torch.empty((B, ws.n_dirs, ws.bins), dtype=torch.float32, device=dev)
+            sp = stream.cuda_stream
+
+            def step(k):
+                ws.process_device(pin.data_ptr() + (k % 2) * B * ws.packed_bytes, B, out.data_ptr(), sp)
+
+            with torch.cuda.stream(stream):
+                step(1)
+                stream.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for k in range(args.sweep_steps):
+                    step(k)
+                e1.record(stream)
+                e1.synchronize()
+                ms = e0.elapsed_time(e1) / args.sweep_steps
+                ws.set_profiling(True)
+                step(0)
+                stream.synchronize()
+                st = ws.stage_times()
+                ws.set_profiling(False)
+            kf = kernel_flops(ws.dims)
+            env_tf = kf["envelope"] * B / (st["envelope"] * 1e-3) / 1e12
+            pts.append({
+                "grid": grid, "n_directions": n, "max_range_m": mr, "frames": d["frames"], "env_fft": N,
+                "range_bins": d["range_bins"], "batch": B, "value": B / (ms * 1e-3), "unit": UNIT,
+                "ms_per_capture": ms / B, "stage_ms_per_capture": {k: v / B for k, v in st.items()},
+                "envelope_frac": env_tf / peak, "setup_s": setup_s,
+            })
+            del ws, pin, out
+            torch.cuda.empty_cache()
+    return {"points": pts, "steps": args.sweep_steps,
+            "what": "device path (sn_workspace_process_device), GPU-synthesised captures (sn_synthesize_device); "
+                    "frac: envelope stage vs the live FMA peak"}
+
+
 def stream_bench(sn, cfg, ws, pool_h, args, L, C):
-    """8 sensors (serials 1..8) x N/8 time-synchronised measurements as wire
-    frames through sn_pool (2 workers x max_batch 8 on one GPU): sustained
-    throughput unthrottled, then per-frame latency (submit -> released) at the
-    10 Hz-per-sensor rate of configs[3] (80 frames/s offered), over a bounded
-    sample."""
+    """BASELINE configs[3]: 8 sensors (serials 1..8) x N/8 time-synchronised
+    measurements (default 256 x 8) as wire frames through sn_pool (2 workers
+    x max_batch 8 on one GPU): sustained throughput unthrottled, then
+    per-frame latency (submit -> released) at the 10 Hz-per-sensor rate
+    (80 frames/s offered) over a bounded paced sample."""
     n = args.stream_frames
     frames = []
     for k in range(n):
@@ -270,8 +388,8 @@ def stream_bench(sn, cfg, ws, pool_h, args, L, C):
         poll()
     feeder.join()
     sustained = n / (time.perf_counter() - t0)
-    # paced: 80 frames/s offered for ~2 s; latency = release time - submit time
-    paced_n = 160
+    # paced: 80 frames/s offered; latency = release time - submit time
+    paced_n = args.paced_frames
     sub_t = {}
     done = []
 
@@ -293,7 +411,7 @@ def stream_bench(sn, cfg, ws, pool_h, args, L, C):
     feeder.join()
     lat = [(t - sub_t[key]) * 1e3 for key, t in done]
     pool.close()
-    return {"frames": n, "sensors": 8, "workers": 2, "max_batch": 8,
+    return {"frames": n, "measurements_per_sensor": n // 8, "sensors": 8, "workers": 2, "max_batch": 8,
             "sustained_value": sustained, "unit": UNIT,
             "paced_offered_per_s": 80, "paced_frames": paced_n,
             "latency_ms_p50": float(np.percentile(lat, 50)), "latency_ms_p99": float(np.percentile(lat, 99)),
@@ -305,6 +423,8 @@ def stream_bench(sn, cfg, ws, pool_h, args, L, C):
 def run_b200(args):
     import torch
     import paper_2208_10839_b200 as sn
+    if args.lib:
+        sn.load_library(args.lib)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -327,29 +447,37 @@ def run_b200(args):
     serial = rank + 1
     pool_h = synth_pool(sn, cfg, serial, pool_n)
     pool = torch.from_numpy(pool_h).to(dev)
-    out = torch.empty((B, ws.n_dirs, ws.bins), dtype=torch.float32, device=dev)
+    outs = [torch.empty((B, ws.n_dirs, ws.bins), dtype=torch.float32, device=dev) for _ in range(2)]
+    out = outs[0]
     stream = torch.cuda.Stream(device=dev)
     sptr = stream.cuda_stream
     nchunks = pool_n // B
 
+    # 360-degree view (configs[2]): the C++ NCCL gather (sn_gather_*) of every
+    # step's energyscapes to rank 0 on its own stream, double-buffered: step
+    # k writes outs[k % 2] while step k - 1's gather reads the other slot
+    vg, views = None, None
+    if dist is not None and args.gather:
+        from paper_2208_10839_b200.distributed import ViewGather
+        vg = ViewGather(ws.n_dirs * ws.bins, B, device=local)
+        if rank == 0:
+            views = [torch.empty((world, B, ws.n_dirs, ws.bins), dtype=torch.float32, device=dev)
+                     for _ in range(2)]
+
     def step(k):
         src = pool[(k % nchunks) * B]
-        ws.process_device(src.data_ptr(), B, out.data_ptr(), sptr)
-
-    gather_buf = None
-    if dist is not None and args.gather:
-        gather_buf = [torch.empty_like(out) for _ in range(world)] if rank == 0 else None
-
-    def gather():
-        if dist is not None and args.gather:
-            with torch.cuda.stream(stream):
-                dist.gather(out, gather_buf if rank == 0 else None, dst=0)
+        slot = k % 2
+        if vg is not None:
+            vg.wait(slot, sptr)  # the slot's previous gather has read outs[slot]
+        ws.process_device(src.data_ptr(), B, outs[slot].data_ptr(), sptr)
+        if vg is not None:
+            ids = [(serial, 100000 * k, k)] * B  # one trigger per step (sync.hpp:16-19)
+            vg.start(slot, outs[slot].data_ptr(), ids, views[slot].data_ptr() if rank == 0 else 0, sptr)
 
     # ---- warm-up ----------------------------------------------------------
     with torch.cuda.stream(stream):
         for k in range(args.warmup):
             step(k)
-            gather()
     torch.cuda.synchronize(dev)
 
     # ---- device-resident timed region ---------------------------------------
@@ -363,12 +491,22 @@ def run_b200(args):
             e0.record(stream)
             for k in range(args.steps):
                 step(k)
-                gather()
+            if vg is not None:  # the last steps' gathers belong to the timed region
+                for sl in range(2):
+                    vg.wait(sl, sptr)
             e1.record(stream)
         torch.cuda.synchronize(dev)
     if dist is not None:
         dist.barrier()
     elapsed_ms = e0.elapsed_time(e1)
+    gather_res = None
+    if vg is not None:
+        gather_res = {"ms_last": [vg.elapsed_ms(sl) for sl in range(2)],
+                      "bytes_to_root_per_step": (world - 1) * B * ws.n_dirs * ws.bins * 4,
+                      "what": "sn_gather (C++ NCCL send/recv to rank 0, own stream, double-buffered view slots)"}
+        if rank == 0:
+            ids, ok = vg.ids((args.steps - 1) % 2)
+            gather_res["triggers_synchronized"] = ok
     launches = ws.last_launches() * args.steps
     if dist is not None:
         t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
@@ -532,6 +670,7 @@ def run_b200(args):
             "hbm_compulsory_gbs": bytes_per * value / world / 1e9,
         },
         "stream_pool": stream_res,
+        "gather": gather_res,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
@@ -540,6 +679,15 @@ def run_b200(args):
             line["cpu_baseline"] = cpu_baseline(cfg, args.grid, args.cpu_calls)
         except Exception as e:  # the GPU number stands on its own
             line["cpu_baseline"] = {"error": str(e)}
+        if args.cpu_latency_calls > 0:
+            try:
+                cl = cpu_latency(args.grid, args.cpu_latency_calls)
+                line["cpu_baseline"]["latency_ms"] = cl
+                line["latency_ms"]["cpu_reference_p50"] = {k: cl[k]["p50"] for k in ("threads_2", "threads_nproc")}
+            except Exception as e:
+                line["cpu_baseline"]["latency_ms"] = {"error": str(e)}
+    if rank == 0 and world == 1 and not args.no_sweep:
+        line["sweep"] = sweep(sn, args, local, peak)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:

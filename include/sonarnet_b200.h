@@ -137,7 +137,11 @@ typedef struct sn_workspace sn_workspace;
 typedef enum sn_stage {
     SN_STAGE_DEMOD = 0, /* 32 x demod_samples f64 (demod_buf)   */
     SN_STAGE_PREMF = 1, /* 32 x mf_samples f64    (mf_buf)      */
-    SN_STAGE_FILT = 2   /* 32 x mf_samples f64    (filt_buf)    */
+    SN_STAGE_FILT = 2,  /* 32 x mf_samples f64    (filt_buf)    */
+    SN_STAGE_BEAMS = 3  /* n_directions x mf_samples: the hot path's delay-and-sum
+                           of that measurement (beamform_into, pipeline.cpp:432-446),
+                           direction order, f64 (f32 beams widened in F32 mode);
+                           recomputed on demand by the same kernels (deterministic) */
 } sn_stage;
 
 /* ---- library ---------------------------------------------------------- */
@@ -156,6 +160,10 @@ sn_status sn_default_array(uint64_t seed, double* mic_xyz_out);
 /* geometry.cpp:181-235 direction_grid(kind) -> n x (az, el) */
 sn_status sn_direction_grid(int32_t grid_kind, double* out, uint64_t capacity,
                             uint64_t* n_out);
+/* The Fibonacci lattice of hemisphere3000 (geometry.cpp:206-229) with n
+ * points instead of 3000 (n = 3000 reproduces the built-in grid exactly):
+ * n x (az, el) into `out`; the configs[4] sweep's dense custom grids. */
+sn_status sn_fibonacci_hemisphere(uint64_t n, double* out, uint64_t capacity);
 /* pipeline.cpp:60-92 PipelineConfig::validate + derived sizes. */
 sn_status sn_config_dims(const sn_pipeline_config* cfg, sn_dims* dims);
 /* synth.cpp:116-134 synthesize_measurement: packed bytes of one capture.
@@ -179,6 +187,22 @@ sn_status sn_synthesize_device(const sn_pipeline_config* cfg, const sn_scene* sc
  * SN_ERR_CUDA. max_batch: largest batch a single process call may carry. */
 sn_status sn_workspace_create(const sn_pipeline_config* cfg, int device, uint64_t max_batch,
                               sn_workspace** out);
+/* Device-side choices of a workspace (no effect on results beyond the
+ * per-stage tolerances of DESIGN.md §5); zero-initialised = defaults. */
+typedef enum sn_beamformer_kind {
+    SN_BEAMFORMER_TENSOR_CORE = 0, /* tcgen05 int8 delay-and-sum (default)        */
+    SN_BEAMFORMER_CUDA_CORE = 1    /* FP64 CUDA-core tiles, bit-identical beams   */
+} sn_beamformer_kind;
+typedef struct sn_workspace_options {
+    int32_t beamformer;          /* sn_beamformer_kind                                 */
+    int32_t tc_tile_n;           /* tensor-core tile width: 0 = 96; 64, 96 or 128      */
+    uint64_t beam_budget_bytes;  /* 0 = 4 GiB: device bytes of the beam ring (beams +
+                                    digit planes of the captures one chunk of a batch
+                                    holds); larger grids/windows run more chunks      */
+} sn_workspace_options;
+/* sn_workspace_create with options (NULL = defaults). */
+sn_status sn_workspace_create_ex(const sn_pipeline_config* cfg, int device, uint64_t max_batch,
+                                 const sn_workspace_options* options, sn_workspace** out);
 void sn_workspace_destroy(sn_workspace* ws);
 sn_status sn_workspace_dims(const sn_workspace* ws, sn_dims* dims);
 
@@ -300,6 +324,45 @@ sn_status sn_pool_poll_view(sn_pool* pool, int timeout_ms, const uint8_t** data,
 /* stats: submitted, completed, discarded (CRC), workers */
 sn_status sn_pool_stats(sn_pool* pool, uint64_t* stats4);
 uint64_t sn_pool_frame_bytes(const sn_pool* pool);
+
+/* ---- multi-sensor 360-degree view (BASELINE configs[2]) ---
+ * One sensor per GPU, one process per GPU; the energyscapes of a trigger are
+ * gathered to rank 0 over NCCL (bound at run time from libnccl.so.2) on the
+ * gather's own stream, into one of two view slots (double buffering: step k's
+ * gather overlaps step k + 1). The ids travel with the images; a trigger is
+ * the same (timestamp_us, seq) on every sensor (nodes/sync.hpp:16-19).
+ * Replaces the reference's per-sensor fan-out of images to subscribers
+ * (central_node.cpp:272-336) for the co-located 8-GPU network. */
+#define SN_GATHER_ID_BYTES 128 /* NCCL_UNIQUE_ID_BYTES */
+typedef struct sn_frame_id {
+    uint32_t sensor_serial;
+    uint32_t reserved;
+    uint64_t timestamp_us;
+    uint64_t seq;
+} sn_frame_id;
+typedef struct sn_gather sn_gather;
+/* rank 0 creates the id and shares it out of band (e.g. a TCP store). */
+sn_status sn_gather_unique_id(uint8_t* id_out /* SN_GATHER_ID_BYTES */);
+/* collective over the `world` ranks; image_floats = n_dirs * range_bins;
+ * max_count = images per rank per gather. */
+sn_status sn_gather_create(int rank, int world, const uint8_t* id, int device, uint64_t image_floats,
+                           uint64_t max_count, sn_gather** out);
+void sn_gather_destroy(sn_gather* g);
+/* After the work already enqueued on `stream` (the producer of d_images),
+ * gather `count` images (count x image_floats f32, device) and their ids
+ * (host) from every rank into slot `slot` (0/1) of rank 0's d_view (device,
+ * world x count x image_floats, rank-major; ignored elsewhere). Returns once
+ * enqueued; collective: every rank calls it with the same slot and count. */
+sn_status sn_gather_start(sn_gather* g, int slot, const float* d_images, const sn_frame_id* ids, uint64_t count,
+                          float* d_view, void* stream);
+/* Make `stream` wait for slot's last gather (NULL: block the host) — call
+ * before overwriting the images or reading the view of that slot. */
+sn_status sn_gather_wait(sn_gather* g, int slot, void* stream);
+/* rank 0: the gathered ids of slot (world x count, rank-major, blocks until
+ * done) and whether every rank's image i belongs to the same trigger. */
+sn_status sn_gather_ids(sn_gather* g, int slot, sn_frame_id* out, uint64_t capacity, int32_t* synchronized);
+/* device ms of slot's last gather (its own stream, CUDA events). */
+sn_status sn_gather_elapsed(sn_gather* g, int slot, float* ms);
 
 /* FMA-throughput microbenchmark on `device` (TFLOP/s, FMA = 2 flops); the
  * roofline denominator for CUDA-core kernels (no tensor cores involved). */

@@ -26,14 +26,14 @@ from typing import Iterable, List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# SNB_LIB: developer override (A/B builds of the same sources); default in-tree build
-LIB_PATH = os.environ.get("SNB_LIB") or os.path.join(_HERE, "_lib", "libsonarnet_b200.so")
+LIB_PATH = os.path.join(_HERE, "_lib", "libsonarnet_b200.so")
 
 __all__ = [
     "GridKind", "Precision", "PipelineConfig", "RawMeasurement", "AcousticImage", "Reflector",
     "Scene", "Workspace", "default_pipeline_config", "direction_grid", "default_array",
     "synthesize_measurement", "SonarError", "ConfigError", "ArgumentError", "DecodeError",
     "IoError", "CudaError", "lib", "crc32", "measurement_frame", "CentralPool", "synthesize_device",
+    "fibonacci_hemisphere", "Beamformer", "load_library",
 ]
 
 
@@ -76,6 +76,15 @@ class GridKind(enum.IntEnum):  # geometry.hpp:65
 class Precision(enum.IntEnum):
     f64 = 0
     f32 = 1
+
+
+class Beamformer(enum.IntEnum):  # sn_beamformer_kind
+    tensor_core = 0
+    cuda_core = 1
+
+
+class _Options(C.Structure):  # sn_workspace_options
+    _fields_ = [("beamformer", C.c_int32), ("tc_tile_n", C.c_int32), ("beam_budget_bytes", C.c_uint64)]
 
 
 # ---------------------------------------------------------------------------
@@ -135,6 +144,11 @@ class _Scene(C.Structure):
                 ("noise_rms", C.c_double), ("seed", C.c_uint64)]
 
 
+class FrameId(C.Structure):  # sn_frame_id: one image's trigger identity (sync.hpp:16-19)
+    _fields_ = [("sensor_serial", C.c_uint32), ("reserved", C.c_uint32), ("timestamp_us", C.c_uint64),
+                ("seq", C.c_uint64)]
+
+
 _lib: Optional[C.CDLL] = None
 
 STAGES = ("demod", "premf", "matched_filter", "beamform", "envelope")
@@ -144,6 +158,16 @@ class _BfInfo(C.Structure):  # sn_beamformer_info
     _fields_ = [("kind", C.c_int32), ("clusters", C.c_int32), ("sum_R", C.c_int64), ("max_R", C.c_int32),
                 ("ntiles", C.c_int32), ("slices", C.c_int32), ("m", C.c_int32), ("n", C.c_int32),
                 ("k", C.c_int32)]
+
+
+def load_library(path: str) -> C.CDLL:
+    """Bind another build of the same sources (developer A/B builds) instead
+    of the in-tree library; call before anything else touches lib()."""
+    global _lib, LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("the library is already loaded")
+    LIB_PATH = path
+    return lib()
 
 
 def lib() -> C.CDLL:
@@ -163,6 +187,8 @@ def lib() -> C.CDLL:
     L.sn_config_dims.argtypes = [C.POINTER(_Config), C.POINTER(_Dims)]
     L.sn_synthesize_packed.argtypes = [C.POINTER(_Config), C.POINTER(_Scene), vp, u64]
     L.sn_workspace_create.argtypes = [C.POINTER(_Config), C.c_int, u64, C.POINTER(vp)]
+    L.sn_workspace_create_ex.argtypes = [C.POINTER(_Config), C.c_int, u64, C.POINTER(_Options), C.POINTER(vp)]
+    L.sn_fibonacci_hemisphere.argtypes = [u64, vp, u64]
     L.sn_workspace_destroy.argtypes = [vp]
     L.sn_workspace_dims.argtypes = [vp, C.POINTER(_Dims)]
     L.sn_workspace_process.argtypes = [vp, C.POINTER(_Measurement), vp]
@@ -200,6 +226,13 @@ def lib() -> C.CDLL:
     L.sn_workspace_image_frame_bytes.argtypes = [vp]
     L.sn_workspace_process_frames.argtypes = [vp, C.POINTER(C.c_void_p), C.POINTER(u64), u64, vp, u64,
                                               C.POINTER(u64), C.POINTER(C.c_int32)]
+    L.sn_gather_unique_id.argtypes = [vp]
+    L.sn_gather_create.argtypes = [C.c_int, C.c_int, vp, C.c_int, u64, u64, C.POINTER(vp)]
+    L.sn_gather_destroy.argtypes = [vp]
+    L.sn_gather_start.argtypes = [vp, C.c_int, vp, C.POINTER(FrameId), u64, vp, vp]
+    L.sn_gather_wait.argtypes = [vp, C.c_int, vp]
+    L.sn_gather_ids.argtypes = [vp, C.c_int, C.POINTER(FrameId), u64, C.POINTER(C.c_int32)]
+    L.sn_gather_elapsed.argtypes = [vp, C.c_int, C.POINTER(C.c_float)]
     _lib = L
     return L
 
@@ -301,6 +334,13 @@ def direction_grid(kind: GridKind) -> np.ndarray:
     _check(lib().sn_direction_grid(int(kind), None, 0, C.byref(n)))
     out = np.zeros((n.value, 2), np.float64)
     _check(lib().sn_direction_grid(int(kind), out.ctypes.data, n.value, C.byref(n)))
+    return out
+
+
+def fibonacci_hemisphere(n: int) -> np.ndarray:
+    """geometry.cpp:206-229 with n points (n = 3000: hemisphere3000) — n x (az, el)."""
+    out = np.zeros((int(n), 2), np.float64)
+    _check(lib().sn_fibonacci_hemisphere(int(n), out.ctypes.data, int(n)))
     return out
 
 
@@ -469,14 +509,18 @@ class Workspace:
 
     device=None picks the current torch device if torch is initialised, else 0;
     device=-1 builds the host tables only (no GPU needed; process raises).
+    beamformer / tc_tile_n / beam_budget_bytes: sn_workspace_options.
     """
 
-    def __init__(self, cfg: PipelineConfig, device: Optional[int] = 0, max_batch: int = 1):
+    def __init__(self, cfg: PipelineConfig, device: Optional[int] = 0, max_batch: int = 1,
+                 beamformer: Beamformer = Beamformer.tensor_core, tc_tile_n: int = 0,
+                 beam_budget_bytes: int = 0):
         self._cfg = cfg
         st, _k = cfg._struct()
         h = C.c_void_p()
         dev = 0 if device is None else int(device)
-        _check(lib().sn_workspace_create(C.byref(st), dev, max(1, int(max_batch)), C.byref(h)))
+        opt = _Options(int(beamformer), int(tc_tile_n), int(beam_budget_bytes))
+        _check(lib().sn_workspace_create_ex(C.byref(st), dev, max(1, int(max_batch)), C.byref(opt), C.byref(h)))
         self._h = h
         d = _Dims()
         _check(lib().sn_workspace_dims(h, C.byref(d)))
@@ -618,7 +662,9 @@ class Workspace:
         return dict(zip(STAGES, map(float, out)))
 
     def stage(self, which: int, item: int = 0) -> np.ndarray:
+        """Stage buffers of capture `item` of the last call: 0 demod, 1 pre-MF,
+        2 matched filter (32 x samples), 3 beams (n_dirs x mf_samples)."""
         L = self.dims["demod_samples"] if which == 0 else self.dims["mf_samples"]
-        out = np.empty((32, L), np.float64)
+        out = np.empty((self.n_dirs if which == 3 else 32, L), np.float64)
         _check(lib().sn_workspace_stage(self._h, which, item, out.ctypes.data, out.size))
         return out

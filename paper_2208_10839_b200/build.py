@@ -32,7 +32,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr
                      "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v"]
 
 CU_SOURCES = ["kernels.cu", "beamform_tc.cu", "frames.cu", "synth.cu", "sn_api.cu"]
-CPP_SOURCES = ["plan.cpp", "pool.cpp"]
+CPP_SOURCES = ["plan.cpp", "pool.cpp", "gather.cpp"]
 HEADERS = ["fft.cuh", "kernels.cuh", "plan.hpp"]
 
 
@@ -72,7 +72,7 @@ def build(verbose: bool = False) -> str:
                     print(out)
             objs.append(o)
         if _newer(SO, objs):
-            _run([NVCC, *ARCH, "-shared", "-o", SO, *objs, "-lpthread"], log)
+            _run([NVCC, *ARCH, "-shared", "-o", SO, *objs, "-lpthread", "-ldl"], log)
     return SO
 
 

@@ -513,21 +513,16 @@ void launch_digits(const DigitArgs& a, int batch, cudaStream_t s) {
     k_digits<<<dim3(2 * nblk, a.clusters, batch), 128, 0, s>>>(a);
 }
 
-void launch_beamform_tc(const TcArgs& a, const TcSched& sched, int grid, cudaStream_t s) {
+cudaError_t launch_beamform_tc(const TcArgs& a, const TcSched& sched, int grid, cudaStream_t s) {
     const size_t smem = beamform_tc_smem_bytes(a.rmax, a.pad, a.n);
     const void* fn = a.n == 128 ? (const void*)k_beamform_tc<128>
                    : a.n == 96  ? (const void*)k_beamform_tc<96>
                                 : (const void*)k_beamform_tc<64>;
-    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) {
-        fprintf(stderr, "k_beamform_tc: %zu bytes of shared memory: %s\n", smem, cudaGetErrorString(e));
-        return;
-    }
+    set_smem(fn, smem);
     if (a.n == 128) k_beamform_tc<128><<<grid, kTcThreads, smem, s>>>(a, sched);
     else if (a.n == 96) k_beamform_tc<96><<<grid, kTcThreads, smem, s>>>(a, sched);
     else k_beamform_tc<64><<<grid, kTcThreads, smem, s>>>(a, sched);
-    const cudaError_t le = cudaPeekAtLastError();
-    if (le != cudaSuccess) fprintf(stderr, "k_beamform_tc launch: %s\n", cudaGetErrorString(le));
+    return cudaPeekAtLastError();
 }
 
 } // namespace snb

@@ -1,8 +1,13 @@
 // Hot-path kernels; see kernels.cuh for the stage map and layouts.
 #include "fft.cuh"
 #include "kernels.cuh"
+#include "plan.hpp"
 
 #include <cstdio>
+#include <mutex>
+#include <string>
+#include <map>
+#include <utility>
 
 #ifndef SNB_ENV_MINB
 #define SNB_ENV_MINB 2 // envelope CTAs per SM the register budget is sized for
@@ -676,8 +681,25 @@ size_t fft_smem_bytes(int n, int real_bytes) {
     return (size_t)(M + M / 16) * 2 * real_bytes;
 }
 
-static void set_smem(const void* fn, size_t smem) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+// Dynamic shared-memory opt-in of a kernel, raised once per (kernel, size)
+// (workspaces on several host threads share the table); a failure is thrown
+// as SN_ERR_CUDA through the C ABI instead of surfacing as a launch error.
+void set_smem(const void* fn, size_t smem) {
+    static std::mutex m;
+    static std::map<std::pair<int, const void*>, size_t> done; // per device: the attribute is per context
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_pair(dev, fn);
+    std::lock_guard<std::mutex> lk(m);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= smem) return;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error(SN_ERR_CUDA, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize = " + std::to_string(smem) +
+                                     "): " + cudaGetErrorString(e));
+    }
+    done[key] = smem;
 }
 
 void launch_demod(const DemodArgs& a, int grid_x, size_t smem, cudaStream_t s) {

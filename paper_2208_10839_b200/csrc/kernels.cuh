@@ -196,10 +196,12 @@ struct TcArgs {
 constexpr int kTcMaxGrid = 512;
 struct TcSched { int start[kTcMaxGrid + 1]; }; // CTA k processes tiles [start[k], start[k+1])
 void launch_digits(const DigitArgs& a, int batch, cudaStream_t s);
-void launch_beamform_tc(const TcArgs& a, const TcSched& sched, int grid, cudaStream_t s);
+cudaError_t launch_beamform_tc(const TcArgs& a, const TcSched& sched, int grid, cudaStream_t s);
 size_t beamform_tc_smem_bytes(int rmax, int pad, int tn);
 
 size_t demod_smem_bytes(int octets, int words);
+// raise a kernel's dynamic shared-memory limit (cached; throws Error(SN_ERR_CUDA))
+void set_smem(const void* fn, size_t smem);
 size_t fft_smem_bytes(int n, int real_bytes);
 
 } // namespace snb

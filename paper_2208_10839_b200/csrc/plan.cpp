@@ -212,6 +212,31 @@ void default_array(uint64_t seed, double* xyz) { // geometry.cpp:69-96
     }
 }
 
+// Fibonacci lattice on the forward hemisphere (geometry.cpp:206-229 with the
+// point count n free: the reference's hemisphere3000 is n = 3000), sorted by
+// (elevation, azimuth) as the reference sorts it (geometry.cpp:222-226).
+std::vector<double> fibonacci_hemisphere(uint64_t n) {
+    if (n == 0) config_error("fibonacci_hemisphere: n must be >= 1");
+    const double golden = kPi * (3.0 - std::sqrt(5.0));
+    std::vector<std::pair<double, double>> d; // (el, az)
+    d.reserve(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        const double x = (static_cast<double>(i) + 0.5) / static_cast<double>(n);
+        const double r = std::sqrt(1.0 - x * x);
+        const double phi = golden * static_cast<double>(i);
+        const double y = r * std::cos(phi), z = r * std::sin(phi);
+        d.emplace_back(std::asin(std::clamp(z, -1.0, 1.0)), std::atan2(y, x));
+    }
+    std::sort(d.begin(), d.end());
+    std::vector<double> out;
+    out.reserve(2 * n);
+    for (const auto& [el, az] : d) {
+        out.push_back(az);
+        out.push_back(el);
+    }
+    return out;
+}
+
 std::vector<double> direction_grid(int kind) { // geometry.cpp:181-235
     std::vector<double> out;
     switch (kind) {
@@ -234,25 +259,7 @@ std::vector<double> direction_grid(int kind) { // geometry.cpp:181-235
             }
             break;
         }
-        case SN_GRID_HEMISPHERE3000: {
-            // Fibonacci lattice on the forward hemisphere, sorted (el, az).
-            constexpr int n = 3000;
-            const double golden = kPi * (3.0 - std::sqrt(5.0));
-            std::vector<std::pair<double, double>> d; // (el, az)
-            for (int i = 0; i < n; ++i) {
-                const double x = (static_cast<double>(i) + 0.5) / n;
-                const double r = std::sqrt(1.0 - x * x);
-                const double phi = golden * static_cast<double>(i);
-                const double y = r * std::cos(phi), z = r * std::sin(phi);
-                d.emplace_back(std::asin(std::clamp(z, -1.0, 1.0)), std::atan2(y, x));
-            }
-            std::sort(d.begin(), d.end());
-            for (const auto& [el, az] : d) {
-                out.push_back(az);
-                out.push_back(el);
-            }
-            break;
-        }
+        case SN_GRID_HEMISPHERE3000: out = fibonacci_hemisphere(3000); break;
         default: config_error("direction_grid: custom grids are built from explicit lists");
     }
     return out;

@@ -21,6 +21,9 @@ struct Error : std::runtime_error {
     sn_status status;
     Error(sn_status s, const std::string& what) : std::runtime_error(what), status(s) {}
 };
+// message returned by sn_last_error() on this thread (sn_api.cu)
+void set_last_error(const std::string& m);
+
 [[noreturn]] inline void config_error(const std::string& m) { throw Error(SN_ERR_CONFIG, m); }
 [[noreturn]] inline void argument_error(const std::string& m) { throw Error(SN_ERR_ARGUMENT, m); }
 [[noreturn]] inline void decode_error(const std::string& m) { throw Error(SN_ERR_DECODE, m); }
@@ -69,6 +72,7 @@ std::vector<double> design_lowpass(double cutoff_hz, double sample_rate, int tap
 int decimation_filter_taps(int factor);
 void default_array(uint64_t seed, double* xyz96);
 std::vector<double> direction_grid(int kind); // n x (az, el)
+std::vector<double> fibonacci_hemisphere(uint64_t n); // n x (az, el), geometry.cpp:206-229
 void default_config(int kind, sn_pipeline_config* cfg);
 
 // synth.cpp:116-134: packed bytes of one capture (frame-major, MSB first).

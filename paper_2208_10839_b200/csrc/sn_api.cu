@@ -109,6 +109,8 @@ std::vector<double2> twiddles_small() {
 
 } // namespace
 
+void snb::set_last_error(const std::string& m) { g_last_error = m; }
+
 struct sn_workspace {
     Plan plan;
     int device = -1;
@@ -151,7 +153,12 @@ struct sn_workspace {
     double* d_mf = nullptr;
     double* d_filt = nullptr;
     float* d_filt32 = nullptr;
+    // beam ring: the per-direction stage (digit planes, delay-and-sum,
+    // envelope) runs over chunks of at most `chunk_cap` captures of a batch,
+    // so its buffers are bounded by the beam budget instead of growing as
+    // max_batch x n_dirs x N (30k directions at 10 m: 3.9 GB per capture)
     void* d_beams = nullptr;
+    uint64_t chunk_cap = 1, beam_budget = 0;
     int32_t* d_order = nullptr;
     int32_t* d_shifts_slot = nullptr;
 
@@ -308,7 +315,14 @@ struct sn_workspace {
             d_filt32 = dmalloc<float>(B * kCh * lp, n);
             ck(cudaMemsetAsync(d_filt32, 0, B * kCh * lp * sizeof(float), stream), "memset");
         }
-        const size_t beam_bytes = B * s.n_dirs * s.env_fft * (f32 ? sizeof(float) : sizeof(double));
+        {
+            // captures per chunk: as many as the budget holds (beams + digit
+            // planes per capture), at least one
+            const uint64_t per = s.n_dirs * s.env_fft * (f32 ? sizeof(float) : sizeof(double)) +
+                                 (tc ? (uint64_t)tc_clusters * 12 * tc_rows * 16 + (uint64_t)kCh * s.mf_len * 8 : 0);
+            chunk_cap = std::max<uint64_t>(1, std::min<uint64_t>(B, beam_budget / per));
+        }
+        const size_t beam_bytes = chunk_cap * s.n_dirs * s.env_fft * (f32 ? sizeof(float) : sizeof(double));
         d_beams = dmalloc<uint8_t>(beam_bytes, n);
         ck(cudaMemsetAsync(d_beams, 0, beam_bytes, stream), "memset");
         d_order = dmalloc<int32_t>(s.n_dirs, n);
@@ -533,9 +547,8 @@ struct sn_workspace {
     // SNB_BEAMFORMER=tiles selects the CUDA-core tiled kernel instead.
     std::vector<int32_t> tc_base, tc_start, tc_size;
     std::vector<uint8_t> tc_resid;
-    void plan_tensor_core_beamformer() {
-        const char* env = std::getenv("SNB_BEAMFORMER");
-        tc = !(env && std::string(env) == "tiles");
+    void plan_tensor_core_beamformer(const sn_workspace_options& opt) {
+        tc = opt.beamformer != SN_BEAMFORMER_CUDA_CORE;
         if (!tc) return;
         const Sizes& s = plan.sz;
         tc_R.clear();
@@ -588,8 +601,7 @@ struct sn_workspace {
         // wide tiles (N = 128: 3 TMEM slots, ~1.4x the int8 MMA rate per
         // instruction) when the resident A_r and three B windows fit in
         // shared memory; SNB_TC_N=64 forces the narrow tiles
-        const char* ev = getenv("SNB_TC_N");
-        const int want = ev ? atoi(ev) : 96;
+        const int want = opt.tc_tile_n ? opt.tc_tile_n : 96;
         tc_n = kTcN;
         for (int n : {128, 96})
             if (want >= n && tc_n == kTcN && beamform_tc_smem_bytes(tc_rmax, tc_pad, n) <= 220 * 1024) tc_n = n;
@@ -600,8 +612,8 @@ struct sn_workspace {
     void init_tensor_core_beamformer(int sms) {
         if (!tc) return;
         uint64_t& n = device_allocs;
-        d_planes = dmalloc<int8_t>(max_batch * (uint64_t)tc_clusters * 12 * tc_rows * 16, n);
-        d_dwords = dmalloc<uint2>(max_batch * (uint64_t)kCh * plan.sz.mf_len, n);
+        d_planes = dmalloc<int8_t>(chunk_cap * (uint64_t)tc_clusters * 12 * tc_rows * 16, n);
+        d_dwords = dmalloc<uint2>(chunk_cap * (uint64_t)kCh * plan.sz.mf_len, n);
         d_resid = dmalloc<uint8_t>(tc_resid.size(), n);
         d_tc_R = dmalloc<int32_t>(tc_R.size(), n);
         d_tc_base = dmalloc<int32_t>(tc_base.size(), n);
@@ -677,13 +689,13 @@ struct sn_workspace {
         if (profiling) cudaEventRecord(ev[3], s);
     }
 
-    void enqueue(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s, bool with_envelope = true,
-                 bool with_front = true) {
+    // Delay-and-sum of captures [off, off + count) of the batch (count <=
+    // chunk_cap) into the beam ring (ring position 0 = capture off).
+    void enqueue_beams(uint64_t off, uint64_t count, cudaStream_t s) {
         const Sizes& z = plan.sz;
-        if (with_front) enqueue_front(d_in, 0, count, s);
         if (tc) {
-            DigitArgs dg{d_filt, d_amax, d_tc_base, d_planes, d_dwords, (int64_t)z.mf_len, (int64_t)lp, halo, tc_rows,
-                         tc_pad, tc_clusters};
+            DigitArgs dg{d_filt + off * kCh * lp, d_amax + off, d_tc_base, d_planes, d_dwords, (int64_t)z.mf_len,
+                         (int64_t)lp, halo, tc_rows, tc_pad, tc_clusters};
             launch_digits(dg, (int)count, s);
             TcArgs ta{};
             ta.planes = d_planes;
@@ -692,7 +704,7 @@ struct sn_workspace {
             ta.cl_start = d_tc_start;
             ta.cl_size = d_tc_size;
             ta.rmax = tc_rmax;
-            ta.amax_bits = d_amax;
+            ta.amax_bits = d_amax + off;
             ta.beams = d_beams;
             ta.L = (int64_t)z.mf_len;
             ta.N = (int64_t)z.env_fft;
@@ -704,30 +716,44 @@ struct sn_workspace {
             ta.batch = (int)count;
             ta.f32 = f32 ? 1 : 0;
             ta.n = tc_n;
-            launch_beamform_tc(ta, tc_schedule((int)count), tc_grid, s);
+            ck(launch_beamform_tc(ta, tc_schedule((int)count), tc_grid, s), "tensor-core beamformer");
         } else {
-        BeamArgs ba{};
-        ba.filt = f32 ? (const void*)d_filt32 : (const void*)d_filt;
-        ba.beams = d_beams;
-        ba.shifts = d_shifts_slot;
-        ba.L = (int64_t)z.mf_len;
-        ba.Lp = (int64_t)lp;
-        ba.N = (int64_t)z.env_fft;
-        ba.n_dirs = (int64_t)z.n_dirs;
-        ba.H = halo;
-        ba.T = tile;
-        ba.batch = (int)count;
-        launch_beamform_tiles(ba, f32, s);
+            BeamArgs ba{};
+            ba.filt = f32 ? (const void*)(d_filt32 + off * kCh * lp) : (const void*)(d_filt + off * kCh * lp);
+            ba.beams = d_beams;
+            ba.shifts = d_shifts_slot;
+            ba.L = (int64_t)z.mf_len;
+            ba.Lp = (int64_t)lp;
+            ba.N = (int64_t)z.env_fft;
+            ba.n_dirs = (int64_t)z.n_dirs;
+            ba.H = halo;
+            ba.T = tile;
+            ba.batch = (int)count;
+            launch_beamform_tiles(ba, f32, s);
         }
-        if (profiling) cudaEventRecord(ev[4], s);
-        if (with_envelope) enqueue_envelope(0, count, d_out, s);
+    }
+    uint64_t beam_launches() const { return tc ? 2 : 1; }
+
+    // The device pipeline for `count` captures (<= max_batch): front end for
+    // the batch, then per chunk of the beam ring delay-and-sum + envelope.
+    void enqueue(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s) {
+        enqueue_front(d_in, 0, count, s);
+        uint64_t launches = 3;
+        for (uint64_t off = 0; off < count; off += chunk_cap) {
+            const uint64_t k = std::min(chunk_cap, count - off);
+            if (profiling && off == 0) cudaEventRecord(ev[3], s);
+            enqueue_beams(off, k, s);
+            if (profiling && off + k >= count) cudaEventRecord(ev[4], s);
+            enqueue_envelope(0, k, d_out + off * energy_per, s);
+            launches += beam_launches() + 1;
+        }
         if (profiling) cudaEventRecord(ev[5], s);
         ck(cudaGetLastError(), "kernel launch");
-        last_launches = tc ? 7 : 5;
+        last_launches = launches;
     }
 
-    // Envelope stage for captures [b0, b0 + count) of the batch whose beams
-    // are in d_beams; energies to d_out (capture b0 first).
+    // Envelope stage for ring positions [b0, b0 + count) of the beam ring;
+    // energies to d_out (ring position b0 first).
     void enqueue_envelope(uint64_t b0, uint64_t count, float* d_out, cudaStream_t s) {
         const Sizes& z = plan.sz;
         const size_t rb = f32 ? sizeof(float) : sizeof(double);
@@ -872,6 +898,40 @@ struct sn_workspace {
         return a.type == cudaMemoryTypeHost;
     }
 
+    // Per-direction stage of a block of c captures whose front end is
+    // enqueued on `stream`: per beam-ring chunk the delay-and-sum (on
+    // `stream`), then the envelope in sub-chunks alternating between the two
+    // compute streams so a sub-chunk's CTAs fill the SMs its predecessor's
+    // tail frees; `after(o, k, stream, event)` enqueues the consumer of the
+    // energies of captures [o, o + k) (downloads, frame encoding) on that
+    // sub-chunk's stream and returns its launch count. A later chunk's
+    // delay-and-sum waits until the ring's previous contents are read.
+    template <typename After>
+    uint64_t enqueue_per_direction(uint64_t c, After&& after) {
+        uint64_t nlaunch = 0, ev_j = 0;
+        for (uint64_t o = 0; o < c; o += chunk_cap) {
+            const uint64_t kc = std::min(chunk_cap, c - o);
+            enqueue_beams(o, kc, stream);
+            nlaunch += beam_launches();
+            ck(cudaEventRecord(ev_beams, stream), "event");
+            ck(cudaStreamWaitEvent(s_env2, ev_beams, 0), "wait");
+            const std::vector<uint64_t> chunks = env_chunks(kc);
+            uint64_t off = 0;
+            for (uint64_t j = 0; j < chunks.size(); ++j, ++ev_j) {
+                const uint64_t k = chunks[j];
+                cudaStream_t cs = (j & 1) ? s_env2 : stream;
+                enqueue_envelope(off, k, d_energy + (o + off) * energy_per, cs);
+                nlaunch += 1 + after(o + off, k, cs, ev_done[ev_j % kMaxChunks]);
+                off += k;
+            }
+            if (chunks.size() > 1) {
+                ck(cudaEventRecord(ev_beams, s_env2), "event");
+                ck(cudaStreamWaitEvent(stream, ev_beams, 0), "wait");
+            }
+        }
+        return nlaunch;
+    }
+
     // Host path: H2D of every capture, the device pipeline, D2H of the
     // energyscapes, one synchronisation per max_batch block. A block is cut
     // into up to kMaxChunks chunks pipelined over three streams (H2D, kernels,
@@ -912,25 +972,16 @@ struct sn_workspace {
                 enqueue_front(d_packed + p0 * packed_bytes, p0, p1 - p0, stream);
                 p0 = p1;
             }
-            enqueue(d_packed, c, d_energy, stream, /*with_envelope=*/false, /*with_front=*/false);
-            ck(cudaEventRecord(ev_beams, stream), "event");
-            ck(cudaStreamWaitEvent(s_env2, ev_beams, 0), "wait");
-            const std::vector<uint64_t> chunks = env_chunks(c);
-            const uint64_t nch = chunks.size();
-            uint64_t off = 0;
-            for (uint64_t j = 0; j < nch; ++j) {
-                const uint64_t k = chunks[j]; // captures in chunk j
-                cudaStream_t cs = (j & 1) ? s_env2 : stream;
-                enqueue_envelope(off, k, d_energy + off * energy_per, cs);
-                ck(cudaEventRecord(ev_done[j], cs), "event");
-                ck(cudaStreamWaitEvent(s_d2h, ev_done[j], 0), "wait");
-                float* dst = (out_pinned ? out + done * energy_per : h_out) + off * energy_per;
-                ck(cudaMemcpyAsync(dst, d_energy + off * energy_per, k * energy_per * sizeof(float),
-                                   cudaMemcpyDeviceToHost, s_d2h), "D2H");
-                off += k;
-            }
+            const uint64_t nlaunch = enqueue_per_direction(c, [&](uint64_t o, uint64_t k, cudaStream_t cs, cudaEvent_t ed) {
+                float* d_e = d_energy + o * energy_per;
+                ck(cudaEventRecord(ed, cs), "event");
+                ck(cudaStreamWaitEvent(s_d2h, ed, 0), "wait");
+                float* dst = (out_pinned ? out + done * energy_per : h_out) + o * energy_per;
+                ck(cudaMemcpyAsync(dst, d_e, k * energy_per * sizeof(float), cudaMemcpyDeviceToHost, s_d2h), "D2H");
+                return uint64_t{0};
+            });
             ck(cudaGetLastError(), "kernel launch");
-            last_launches = 3 * parts + (tc ? 3 : 1) + nch;
+            last_launches = 3 * parts + nlaunch;
             ck(cudaStreamSynchronize(s_d2h), "process sync");
             if (!out_pinned) std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
             done += c;
@@ -997,38 +1048,30 @@ struct sn_workspace {
                                 nin, false, d_crc_ok, stream);
             ck(cudaMemcpy2DAsync(d_packed, packed_bytes, d_frames_in + 74, in_frame_stride, packed_bytes, c,
                                  cudaMemcpyDeviceToDevice, stream), "D2D packed");
-            enqueue(d_packed, c, d_energy, stream, /*with_envelope=*/false);
+            enqueue_front(d_packed, 0, c, stream);
             // envelope + frame encode in chunks; each chunk's frames download
             // (D2H stream) while the next chunk computes. D2H straight into the
             // caller's slots when they are page-locked and consecutive.
             const bool direct = out_pinned && batch.back() - batch.front() == c - 1;
             const uint64_t nout = img_frame_len - 4;
             const uint32_t kout = crc_init_term(h_crc_shift.data(), nout);
-            const std::vector<uint64_t> chunks = env_chunks(c);
-            const uint64_t nch = chunks.size();
-            uint64_t off = 0;
-            ck(cudaEventRecord(ev_beams, stream), "event");
-            ck(cudaStreamWaitEvent(s_env2, ev_beams, 0), "wait");
-            for (uint64_t j = 0; j < nch; ++j) {
-                const uint64_t k = chunks[j];
-                cudaStream_t cs = (j & 1) ? s_env2 : stream;
-                enqueue_envelope(off, k, d_energy + off * energy_per, cs);
+            enqueue_per_direction(c, [&](uint64_t off, uint64_t k, cudaStream_t cs, cudaEvent_t ed) {
                 ImageFrameArgs ia{d_energy + off * energy_per, d_img_tpl, d_ids + off,
                                   d_frames_out + off * img_frame_stride, d_crc_acc + max_batch + off, energy_per,
                                   img_tpl_len, img_frame_len, img_frame_stride};
                 launch_encode_image_frames(ia, k, ct, cs);
                 launch_crc_finalize(d_crc_acc + max_batch + off, kout, k, d_frames_out + off * img_frame_stride,
                                     img_frame_stride, nout, true, nullptr, cs);
-                ck(cudaEventRecord(ev_done[j], cs), "event");
-                ck(cudaStreamWaitEvent(s_d2h, ev_done[j], 0), "wait");
+                ck(cudaEventRecord(ed, cs), "event");
+                ck(cudaStreamWaitEvent(s_d2h, ed, 0), "wait");
                 uint8_t* dst = direct ? out + (batch.front() + off) * slot : h_frames_out + off * img_frame_len;
                 const uint64_t dpitch = direct ? slot : img_frame_len;
                 for (uint64_t i = 0; i < k; ++i) {
                     ck(cudaMemcpyAsync(dst + i * dpitch, d_frames_out + (off + i) * img_frame_stride, img_frame_len,
                                        cudaMemcpyDeviceToHost, s_d2h), "D2H frame");
                 }
-                off += k;
-            }
+                return uint64_t{2};
+            });
             ck(cudaGetLastError(), "frame kernels");
             ck(cudaStreamSynchronize(s_d2h), "frames sync");
             ck(cudaMemcpyAsync(h_crc_ok, d_crc_ok, c * sizeof(int32_t), cudaMemcpyDeviceToHost, stream), "D2H ok");
@@ -1111,6 +1154,30 @@ struct sn_workspace {
         (void)z;
     }
 
+    // SN_STAGE_BEAMS: the delay-and-sum of capture `item` of the last batch,
+    // recomputed into ring position 0 from the retained matched-filter output
+    // (and its block-floating-point scale), slot order -> direction order.
+    void dump_beams(uint64_t item, double* out) {
+        const Sizes& z = plan.sz;
+        DeviceGuard g(device);
+        after_last(stream);
+        enqueue_beams(item, 1, stream);
+        ck(cudaGetLastError(), "beams launch");
+        const size_t rb = f32 ? sizeof(float) : sizeof(double);
+        std::vector<uint8_t> h(z.n_dirs * z.env_fft * rb);
+        ck(cudaMemcpyAsync(h.data(), d_beams, h.size(), cudaMemcpyDeviceToHost, stream), "D2H beams");
+        mark_last(stream);
+        ck(cudaStreamSynchronize(stream), "beams sync");
+        for (uint64_t sl = 0; sl < z.n_dirs; ++sl) {
+            double* dst = out + (uint64_t)plan.order[sl] * z.mf_len;
+            const uint8_t* src = h.data() + sl * z.env_fft * rb;
+            for (uint64_t t = 0; t < z.mf_len; ++t) {
+                if (f32) dst[t] = reinterpret_cast<const float*>(src)[t];
+                else dst[t] = reinterpret_cast<const double*>(src)[t];
+            }
+        }
+    }
+
     void process_device(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s) {
         require_device();
         DeviceGuard g(device);
@@ -1162,6 +1229,15 @@ sn_status sn_direction_grid(int32_t kind, double* out, uint64_t capacity, uint64
     });
 }
 
+sn_status sn_fibonacci_hemisphere(uint64_t n, double* out, uint64_t capacity) {
+    return guarded([&] {
+        if (!out) argument_error("null argument");
+        if (capacity < n) argument_error("buffer too small");
+        const std::vector<double> d = fibonacci_hemisphere(n);
+        std::copy(d.begin(), d.end(), out);
+    });
+}
+
 sn_status sn_default_config(int32_t kind, sn_pipeline_config* cfg, double* dir_buf,
                             uint64_t dir_capacity) {
     return guarded([&] {
@@ -1200,15 +1276,26 @@ sn_status sn_synthesize_packed(const sn_pipeline_config* cfg, const sn_scene* sc
 
 sn_status sn_workspace_create(const sn_pipeline_config* cfg, int device, uint64_t max_batch,
                               sn_workspace** out) {
+    return sn_workspace_create_ex(cfg, device, max_batch, nullptr, out);
+}
+
+sn_status sn_workspace_create_ex(const sn_pipeline_config* cfg, int device, uint64_t max_batch,
+                                 const sn_workspace_options* options, sn_workspace** out) {
     return guarded([&] {
         if (!cfg || !out) argument_error("null argument");
         *out = nullptr;
+        const sn_workspace_options opt = options ? *options : sn_workspace_options{};
+        if (opt.beamformer != SN_BEAMFORMER_TENSOR_CORE && opt.beamformer != SN_BEAMFORMER_CUDA_CORE)
+            argument_error("options: unknown beamformer kind");
+        if (opt.tc_tile_n != 0 && opt.tc_tile_n != 64 && opt.tc_tile_n != 96 && opt.tc_tile_n != 128)
+            argument_error("options: tensor-core tile width must be 64, 96 or 128");
         auto ws = std::make_unique<sn_workspace>();
         ws->plan = make_plan(*cfg);
         ws->device = device;
         ws->max_batch = std::max<uint64_t>(1, max_batch);
         ws->f32 = cfg->precision == SN_PRECISION_F32;
-        ws->plan_tensor_core_beamformer();
+        ws->beam_budget = opt.beam_budget_bytes ? opt.beam_budget_bytes : (uint64_t{4} << 30);
+        ws->plan_tensor_core_beamformer(opt);
         if (cfg->precision != SN_PRECISION_F64 && cfg->precision != SN_PRECISION_F32) {
             config_error("pipeline: unknown precision mode");
         }
@@ -1335,6 +1422,11 @@ sn_status sn_workspace_stage(sn_workspace* ws, int32_t stage, uint64_t item, dou
         const Sizes& z = ws->plan.sz;
         const double* src = nullptr;
         uint64_t n = 0;
+        if (stage == SN_STAGE_BEAMS) {
+            if (capacity < z.n_dirs * z.mf_len) argument_error("buffer too small");
+            ws->dump_beams(item, out);
+            return;
+        }
         switch (stage) {
             case SN_STAGE_DEMOD: src = ws->d_demod + item * kCh * z.demod_len; n = kCh * z.demod_len; break;
             case SN_STAGE_PREMF: src = ws->d_mf + item * kCh * z.mf_fft; n = kCh * z.mf_len; break;

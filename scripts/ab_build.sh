@@ -1,7 +1,7 @@
 #!/bin/bash
 # Developer A/B builds: scripts/ab_build.sh NAME "-DMACRO=..." -> paper_2208_10839_b200/_lib/ab/libNAME.so
 # (same sources and flags as paper_2208_10839_b200/build.py plus the extra defines;
-#  select at run time with SNB_LIB=...)
+#  select at run time with bench.py --lib ...)
 set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 C=$ROOT/paper_2208_10839_b200/csrc

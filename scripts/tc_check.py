@@ -28,8 +28,8 @@ for name, cfg in cfgs.items():
     for prec in (0, 1):
         c = cfg.copy(precision=prec)
         m = sn.synthesize_measurement(c, sn.Scene([sn.Reflector(0.8 if name == "tiny" else 1.4, 0.2, 0.1, 0.8)], 0.01, 3))
-        os.environ["SNB_BEAMFORMER"] = "tc"; e_tc = sn.Workspace(c, device=0).process(m).energies
-        os.environ["SNB_BEAMFORMER"] = "tiles"; e_ti = sn.Workspace(c, device=0).process(m).energies
+        e_tc = sn.Workspace(c, device=0).process(m).energies
+        e_ti = sn.Workspace(c, device=0, beamformer=sn.Beamformer.cuda_core).process(m).energies
         want = ref.workspace(to_oracle(po, c)).process(m.packed)
         bad, same = ulp_ok(e_tc, want)
         print(f"{name:9s} prec={prec} tc-vs-ref rel {rel(e_tc, want):.2e} beyond1ulp {bad} same {same:.4f} | "

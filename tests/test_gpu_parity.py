@@ -376,13 +376,11 @@ def test_full_size_batch_properties(gpu):
 # tensor-core delay-and-sum (beamform_tc.cu) against the CUDA-core tiled kernel
 # (channel-order FP64 sums, bit-identical beams) and the reference
 @pytest.mark.parametrize("name", ["small", "az181", "box1850", "hemi3000"])
-def test_tensor_core_beamformer_vs_tiled_and_reference(gpu, po, ref, name, monkeypatch):
+def test_tensor_core_beamformer_vs_tiled_and_reference(gpu, po, ref, name):
     sn = gpu
     cfg = cfg_for(sn, name)
     m = capture(sn, cfg, [(1.1, 0.3, 0.1 if name not in ("small", "az181") else 0.0, 0.7)], 0.01, 13)
-    monkeypatch.setenv("SNB_BEAMFORMER", "tiles")
-    ws_t = sn.Workspace(cfg, device=0)
-    monkeypatch.setenv("SNB_BEAMFORMER", "tc")
+    ws_t = sn.Workspace(cfg, device=0, beamformer=sn.Beamformer.cuda_core)
     ws_c = sn.Workspace(cfg, device=0)
     assert ws_c.last_launches() in (0, 7)
     e_t, e_c = ws_t.process(m).energies, ws_c.process(m).energies
@@ -394,23 +392,20 @@ def test_tensor_core_beamformer_vs_tiled_and_reference(gpu, po, ref, name, monke
 
 
 @pytest.mark.parametrize("tile_n", [64, 96, 128])
-def test_tensor_core_tile_widths(gpu, po, ref, tile_n, monkeypatch):
+def test_tensor_core_tile_widths(gpu, po, ref, tile_n):
     # the three MMA tile widths (N = 64: 8 TMEM slots; 96: 5; 128: 4 slots with
     # Y_hi parked in shared memory) give identical energyscapes (exact integer
     # sums) within one ulp of the reference; a 1-capture and a 3-capture batch
     sn = gpu
     cfg = cfg_for(sn, "box1850")
-    monkeypatch.setenv("SNB_BEAMFORMER", "tc")
-    monkeypatch.setenv("SNB_TC_N", str(tile_n))
-    ws = sn.Workspace(cfg, device=0, max_batch=3)
+    ws = sn.Workspace(cfg, device=0, max_batch=3, tc_tile_n=tile_n)
     assert ws.beamformer_info()["n"] == tile_n
     ms = [capture(sn, cfg, [(1.0 + 0.3 * i, 0.2 - 0.1 * i, 0.1, 0.7)], 0.01, 21 + i, seq=i) for i in range(3)]
     e = np.stack([im.energies for im in ws.process_batch(ms)])
     r = ref.workspace(to_oracle(po, cfg))
     for i in range(3):
         check_f64(e[i], r.process(ms[i].packed))
-    monkeypatch.setenv("SNB_TC_N", "64")
-    base = sn.Workspace(cfg, device=0, max_batch=3)
+    base = sn.Workspace(cfg, device=0, max_batch=3, tc_tile_n=64)
     assert np.array_equal(np.stack([im.energies for im in base.process_batch(ms)]), e)
 
 

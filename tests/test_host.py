@@ -214,5 +214,70 @@ def test_tensor_core_beamformer_schedule(sn, monkeypatch):
         assert math.ceil(n / 128) <= info["clusters"] <= n
         assert 1 <= info["max_R"] <= 40 and info["sum_R"] <= info["clusters"] * info["max_R"]
         assert info["ntiles"] == math.ceil(ws.dims["mf_samples"] / info["n"])
-    monkeypatch.setenv("SNB_BEAMFORMER", "tiles")
-    assert sn.Workspace(sn.default_pipeline_config(2), device=-1).beamformer_info()["kind"] == 0
+    assert sn.Workspace(sn.default_pipeline_config(2), device=-1,
+                        beamformer=sn.Beamformer.cuda_core).beamformer_info()["kind"] == 0
+
+
+# ---- round 2: dense grids, workspace options, bench legs (CPU only) --------
+def test_fibonacci_hemisphere_matches_the_reference_grid(sn, ref):
+    # n = 3000 is the reference's hemisphere3000 (geometry.cpp:206-229), bit for bit
+    g = sn.fibonacci_hemisphere(3000)
+    assert np.array_equal(g, sn.direction_grid(sn.GridKind.hemisphere3000))
+    assert np.array_equal(g, ref.direction_grid(2))
+
+
+@pytest.mark.parametrize("n", [1, 10, 10000, 30000])
+def test_fibonacci_hemisphere_variable_n(sn, n):
+    # restated in numpy (same formula and sort); libm vs numpy trig may differ
+    # in the last place, so 1e-14 rad
+    g = sn.fibonacci_hemisphere(n)
+    i = np.arange(n, dtype=np.float64)
+    x = (i + 0.5) / n
+    r = np.sqrt(1.0 - x * x)
+    phi = np.pi * (3.0 - np.sqrt(5.0)) * i
+    az = np.arctan2(r * np.cos(phi), x)
+    el = np.arcsin(np.clip(r * np.sin(phi), -1, 1))
+    order = np.lexsort((az, el))
+    want = np.stack([az[order], el[order]], 1)
+    assert g.shape == (n, 2)
+    assert np.abs(g - want).max() <= 1e-14
+    assert (np.diff(g[:, 1]) >= 0).all() and (np.abs(g[:, 0]) <= np.pi / 2).all()
+    with pytest.raises(sn.ConfigError):
+        sn.fibonacci_hemisphere(0)
+
+
+def test_sweep_configs_derived_sizes(sn):
+    # frames 53,000 / 144,800 / 276,000; FFT 4096 /
+    # 8192 / 16384; bins 196 / 655 / 1,311 at 1.5 / 5 / 10 m
+    import bench
+    want = {1.5: (53000, 4096, 196), 5.0: (144800, 8192, 655), 10.0: (276000, 16384, 1311)}
+    for grid, nd in (("fib30k", 30000), ("fib10k", 10000), ("az181", 181), ("hemisphere3000", 3000)):
+        for mr, (fr, nfft, bins) in want.items():
+            d = bench.sweep_config(sn, grid, mr, "f64").dims()
+            assert (d["n_directions"], d["frames"], d["env_fft_size"], d["range_bins"]) == (nd, fr, nfft, bins)
+
+
+def test_workspace_options_validated(sn):
+    cfg = sn.default_pipeline_config(sn.GridKind.horizontal90)
+    with pytest.raises(sn.ArgumentError):
+        sn.Workspace(cfg, device=-1, tc_tile_n=100)
+    with pytest.raises(sn.ArgumentError):
+        sn.Workspace(cfg, device=-1, beamformer=7)
+    for n in (64, 96, 128):
+        assert sn.Workspace(cfg, device=-1, tc_tile_n=n).beamformer_info()["kind"] == 1
+
+
+def test_cpu_latency_leg(ref):
+    # bench.cpp:63-108 protocol through the reference oracle, both thread legs
+    import bench
+    r = bench.cpu_latency("horizontal90", 2)
+    assert r["threads_2"]["threads"] == 2 and r["threads_2"]["n"] == 2
+    assert 0 < r["threads_nproc"]["p50"] and r["threads_2"]["p50"] <= r["threads_2"]["p99"]
+    assert "shim" in r["fft"]
+
+
+def test_trigger_synchronisation_check():
+    from paper_2208_10839_b200.distributed import triggers_synchronized
+    ids = [(1, 100, 7), (1, 200, 8), (2, 100, 7), (2, 200, 8)]  # world 2, 2 images each
+    assert triggers_synchronized(ids, 2)
+    assert not triggers_synchronized([(1, 100, 7), (2, 100, 8)], 2)
