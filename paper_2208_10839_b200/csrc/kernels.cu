@@ -395,30 +395,37 @@ template <typename R>
 __device__ __forceinline__ void fir_polyphase(const R* ph, const R* comp, const EnvArgs& a, float* eo) {
     const int tid = gtid();
     if (a.fir_fast) {
-        const int h = tid >> 7, g = tid & 127;
+        // rounds of 128 output groups (more than one beyond 768 bins: the
+        // 10 m window's 1,311), the exchange scratch reused per round
+        const int h = tid >> 7;
         const int groups = (int)((a.bins + kFirR - 1) / kFirR);
-        const int k0 = g * kFirR;
-        R acc[kFirR];
-#pragma unroll
-        for (int r = 0; r < kFirR; ++r) acc[r] = 0;
         R* red = const_cast<R*>(ph) + kFirD * a.phase_len;
-        if (g < groups) {
-            if (h == 0) fir_half<0>(ph, a.phase_len, k0, acc, comp);
-            else fir_half<1>(ph, a.phase_len, k0, acc, comp);
-            if (h == 1) {
+#pragma unroll 1
+        for (int g0 = 0; g0 < groups; g0 += 128) {
+            const int g = g0 + (tid & 127);
+            const int k0 = g * kFirR, kr = (tid & 127) * kFirR;
+            R acc[kFirR];
 #pragma unroll
-                for (int r = 0; r < kFirR; ++r) red[k0 + r] = acc[r];
-            }
-        }
-        gsync();
-        if (h == 0 && g < groups) {
+            for (int r = 0; r < kFirR; ++r) acc[r] = 0;
+            if (g < groups) {
+                if (h == 0) fir_half<0>(ph, a.phase_len, k0, acc, comp);
+                else fir_half<1>(ph, a.phase_len, k0, acc, comp);
+                if (h == 1) {
 #pragma unroll
-            for (int r = 0; r < kFirR; ++r) {
-                if (k0 + r < a.bins) {
-                    const float v = (float)(acc[r] + red[k0 + r]);
-                    eo[k0 + r] = v > 0.0f ? v : 0.0f;
+                    for (int r = 0; r < kFirR; ++r) red[kr + r] = acc[r];
                 }
             }
+            gsync();
+            if (h == 0 && g < groups) {
+#pragma unroll
+                for (int r = 0; r < kFirR; ++r) {
+                    if (k0 + r < a.bins) {
+                        const float v = (float)(acc[r] + red[kr + r]);
+                        eo[k0 + r] = v > 0.0f ? v : 0.0f;
+                    }
+                }
+            }
+            if (g0 + 128 < groups) gsync();
         }
     } else {
         // generic decimation / tap count: plain polyphase loops, taps in smem

@@ -234,7 +234,12 @@ struct sn_workspace {
     double* d_bf_out = nullptr;
     // optional per-stage timing (events on the launching stream)
     bool profiling = false;
-    cudaEvent_t ev[6] = {};
+    // ev[0..3]: front end boundaries; per beam-ring chunk c: ev_ch[2c]
+    // (delay-and-sum done), ev_ch[2c + 1] (envelope done); stage times sum
+    // over the chunks of the last call
+    cudaEvent_t ev[4] = {};
+    std::vector<cudaEvent_t> ev_ch;
+    uint64_t prof_chunks = 0;
     // graph cache
     cudaGraphExec_t graph = nullptr;
     const uint8_t* g_in = nullptr;
@@ -248,6 +253,9 @@ struct sn_workspace {
         cudaSetDevice(device);
         if (graph) cudaGraphExecDestroy(graph);
         for (cudaEvent_t e : ev) {
+            if (e) cudaEventDestroy(e);
+        }
+        for (cudaEvent_t e : ev_ch) {
             if (e) cudaEventDestroy(e);
         }
         for (int j = 0; j < kMaxChunks; ++j) {
@@ -342,6 +350,8 @@ struct sn_workspace {
         d_tw_env32 = dmalloc<float2>(s.env_fft, n);
         ck(cudaMallocHost(&h_in, B * packed_bytes), "cudaMallocHost");
         for (cudaEvent_t& e : ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+        ev_ch.assign(2 * ((B + chunk_cap - 1) / chunk_cap), nullptr);
+        for (cudaEvent_t& e : ev_ch) ck(cudaEventCreate(&e), "cudaEventCreate");
         ck(cudaMallocHost(&h_out, B * energy_per * sizeof(float)), "cudaMallocHost");
 
         upload(d_lut, plan.demod_lut, stream);
@@ -449,7 +459,7 @@ struct sn_workspace {
             phase_len = std::max(groups * kFirR + fir_q + 1, (int)((s.mf_len + c0) / D) + 1);
             phase_len = std::max(phase_len, (int)s.bins + fir_q + 1);
             phase_len = (phase_len + 1) & ~1; // even: rows stay 16-byte aligned (paired loads)
-            fir_fast = D == kFirD && fir_q == kFirQ && groups <= 128;
+            fir_fast = D == kFirD && fir_q == kFirQ && groups <= 4 * 128;
             init_fir_fft(D, c0);
             if (fir_fast) {
                 for (int p = 0; p < kFirD; ++p) {
@@ -732,22 +742,22 @@ struct sn_workspace {
             launch_beamform_tiles(ba, f32, s);
         }
     }
-    uint64_t beam_launches() const { return tc ? 2 : 1; }
+    uint64_t beam_launches() const { return tc ? 3 : 1; } // k_digit_words + k_digits + k_beamform_tc
 
     // The device pipeline for `count` captures (<= max_batch): front end for
     // the batch, then per chunk of the beam ring delay-and-sum + envelope.
     void enqueue(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s) {
         enqueue_front(d_in, 0, count, s);
-        uint64_t launches = 3;
-        for (uint64_t off = 0; off < count; off += chunk_cap) {
+        uint64_t launches = 3, c = 0;
+        for (uint64_t off = 0; off < count; off += chunk_cap, ++c) {
             const uint64_t k = std::min(chunk_cap, count - off);
-            if (profiling && off == 0) cudaEventRecord(ev[3], s);
             enqueue_beams(off, k, s);
-            if (profiling && off + k >= count) cudaEventRecord(ev[4], s);
+            if (profiling) cudaEventRecord(ev_ch[2 * c], s);
             enqueue_envelope(0, k, d_out + off * energy_per, s);
+            if (profiling) cudaEventRecord(ev_ch[2 * c + 1], s);
             launches += beam_launches() + 1;
         }
-        if (profiling) cudaEventRecord(ev[5], s);
+        prof_chunks = c;
         ck(cudaGetLastError(), "kernel launch");
         last_launches = launches;
     }
@@ -1489,8 +1499,19 @@ sn_status sn_workspace_stage_times(sn_workspace* ws, float* ms5) {
         ws->require_device();
         if (!ws->profiling) argument_error("profiling is not enabled");
         DeviceGuard g(ws->device);
-        ck(cudaEventSynchronize(ws->ev[5]), "event sync");
-        for (int i = 0; i < 5; ++i) ck(cudaEventElapsedTime(&ms5[i], ws->ev[i], ws->ev[i + 1]), "elapsed");
+        if (ws->prof_chunks == 0) argument_error("no profiled device-path call yet");
+        ck(cudaEventSynchronize(ws->ev_ch[2 * ws->prof_chunks - 1]), "event sync");
+        for (int i = 0; i < 3; ++i) ck(cudaEventElapsedTime(&ms5[i], ws->ev[i], ws->ev[i + 1]), "elapsed");
+        ms5[3] = ms5[4] = 0;
+        cudaEvent_t prev = ws->ev[3];
+        for (uint64_t c = 0; c < ws->prof_chunks; ++c) {
+            float a = 0, b = 0;
+            ck(cudaEventElapsedTime(&a, prev, ws->ev_ch[2 * c]), "elapsed");
+            ck(cudaEventElapsedTime(&b, ws->ev_ch[2 * c], ws->ev_ch[2 * c + 1]), "elapsed");
+            ms5[3] += a;
+            ms5[4] += b;
+            prev = ws->ev_ch[2 * c + 1];
+        }
     });
 }
 
