@@ -78,6 +78,7 @@ def parse_args():
                    help="timed reference process() calls per latency leg (bench.cpp:63-108 uses 100)")
     p.add_argument("--no-sweep", action="store_true", help="skip the configs[4] grid x window sweep")
     p.add_argument("--sweep-steps", type=int, default=3)
+    p.add_argument("--only-sweep", action="store_true", help="developer: print the sweep alone")
     p.add_argument("--lib", default=None, help="developer A/B: another build of libsonarnet_b200.so")
     return p.parse_args()
 
@@ -439,6 +440,11 @@ def run_b200(args):
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
+    if args.only_sweep:
+        torch.cuda.set_device(local)
+        peak = sn.measure_fp_peak(local, sn.Precision.f64 if args.precision == "f64" else sn.Precision.f32)
+        print(json.dumps({"sweep": sweep(sn, args, local, peak)}), flush=True)
+        return 0
     cfg = make_config(sn, args.grid, args.precision)
     B = args.batch
     pool_n = max(B, (args.pool // B) * B)

@@ -485,6 +485,49 @@ __device__ __forceinline__ void hilbert_mid_dif_4096(V* buf, const TW& tw, R s) 
     gsync();
 }
 
+// The ODD-bin half of an M = 8192 transform split by one radix-2 DIF stage
+// (k = 2 k' + 1, k' < 4096, held like the M = 4096 forward output): bin k'
+// pairs with 4095 - k' (M - k = 2 (4095 - k') + 1), i.e. row a = k1 + 16 k2
+// with row 255 - a = (15 - k1) + 16 (15 - k2) at k3 -> 15 - k3 (no bin pairs
+// with itself). Lanes l < 16 of warp w take k1 = w, k2 = l, lanes l + 16 the
+// partner rows; t_k = 2 pi (2 k' + 1) / 16384: the row part e^{-2 pi i (2a+1)/16384}
+// comes from the N = 16384 table `h16384`, the k3 part is pi k3 / 16 as above.
+template <typename V, typename TW, typename R>
+__device__ __forceinline__ void hilbert_mid_dif_4096_odd(V* buf, const TW& tw, const V* h16384, R s) {
+    const int t = gtid(), w = t >> 5, l = t & 31;
+    const int k1 = l < 16 ? w : 15 - w;
+    const int k2 = l < 16 ? l : 31 - l;
+    const int src = l ^ 16;
+    const int a = k1 + 16 * k2, row = 256 * k1 + 16 * k2;
+    V z[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) z[r] = buf[pad16(row + r)];
+    dft16<false>(z); // z[out_slot(S)] = O[a + 256 S]
+    const V ha = h16384[2 * a + 1];
+    const R cj = s * ha.x, sj = -s * ha.y;
+    auto cosS = [](int S) { return (R)(S <= 8 ? cos_pi16(S) : -cos_pi16(16 - S)); };
+    auto sinS = [](int S) { return (R)cos_pi16(S <= 8 ? 8 - S : S - 8); };
+    auto shfl = [&](V v) {
+        return V{__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src)};
+    };
+    V nz[16];
+#pragma unroll
+    for (int S = 0; S < 16; ++S) {
+        // partner's O[(255 - a) + 256 (15 - S)]
+        const V pc = shfl(z[out_slot<16>(15 - S)]);
+        const R c = cj * cosS(S) - sj * sinS(S), sn = sj * cosS(S) + cj * sinS(S);
+        const V zk = z[out_slot<16>(S)];
+        nz[S] = V{c * pc.x - sn * zk.y, sn * zk.x - c * pc.y};
+    }
+    V x[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) x[r] = nz[r];
+    dft16<true>(x);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[pad16(row + out_slot<16>(r))] = x[r];
+    gsync();
+}
+
 // inverse stage B (thread (k1, n3)): * conj W256^{k2 n3}, DFT16 over k2, in place
 template <typename V, typename TW>
 __device__ __forceinline__ void dit_pass2_4096(V* buf, const TW& tw) {

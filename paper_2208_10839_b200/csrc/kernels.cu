@@ -358,12 +358,11 @@ __device__ __forceinline__ float fast_sqrt(float x) { return sqrtf(x); }
 // taps (warp-uniform: broadcast) come two per load; the phase loop is rolled
 // (the fully unrolled form overflowed the instruction cache). The upper half
 // hands its partial sums to the lower half through `red`.
-template <int H, typename R>
-__device__ __forceinline__ void fir_half(const R* ph, int phase_len, int k0, R (&acc)[kFirR], const R* staps) {
+template <int P0, int NP, typename R>
+__device__ __forceinline__ void fir_phases(const R* ph, int phase_len, int k0, R (&acc)[kFirR], const R* staps) {
     using V = typename Cx<R>::T;
-    constexpr int P0 = H * (kFirD / 2);
 #pragma unroll 1
-    for (int pp = 0; pp < kFirD / 2; ++pp) {
+    for (int pp = 0; pp < NP; ++pp) {
         const V* row = reinterpret_cast<const V*>(ph + (P0 + pp) * phase_len + k0);
         const V* tp = reinterpret_cast<const V*>(staps + (P0 + pp) * kFirQP);
         R w[kFirR + kFirQ + 1];
@@ -408,8 +407,8 @@ __device__ __forceinline__ void fir_polyphase(const R* ph, const R* comp, const 
 #pragma unroll
             for (int r = 0; r < kFirR; ++r) acc[r] = 0;
             if (g < groups) {
-                if (h == 0) fir_half<0>(ph, a.phase_len, k0, acc, comp);
-                else fir_half<1>(ph, a.phase_len, k0, acc, comp);
+                if (h == 0) fir_phases<0, kFirD / 2>(ph, a.phase_len, k0, acc, comp);
+                else fir_phases<kFirD / 2, kFirD / 2>(ph, a.phase_len, k0, acc, comp);
                 if (h == 1) {
 #pragma unroll
                     for (int r = 0; r < kFirR; ++r) red[kr + r] = acc[r];
@@ -605,6 +604,408 @@ __global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 
         }
         gsync();
     }
+}
+
+// ---------------------------------------------------------------------------
+// k_envelope_pair2048: the envelope for N = 4096 (M = 2048; the 1.5 m window)
+// with TWO beams per 256-thread group, 128 threads per beam, so every pass
+// keeps all threads busy with one 16- or two 8-point butterflies and the
+// register budget of the M = 4096 path (the generic Stockham path left half
+// the threads idle in two passes and spilled 620 B at 128 registers).
+// In-place DIF/DIT pair, indices n = 128 n1 + 8 n2 + n3, k = k1 + 16 k2 + 256 k3:
+//   forward pass 1 (thread m = n mod 128): DFT16 over n1, * W2048^{m k1}, to 128 k1 + m
+//   forward pass 2 (thread (k1, n3)):      DFT16 over n2, * W128^{n3 k2}, to 128 k1 + 8 k2 + n3
+//   middle (thread u: rows a = k1 + 16 k2 and 256 - a, or rows 0 and 128 for u = 0):
+//     DFT8 over n3 -> X[a + 256 k3]; the Hilbert operator pairs bin a + 256 k3
+//     with (256 - a) + 256 (7 - k3), both rows in this thread's registers (no
+//     exchange); inverse DFT8 over k3, in place
+//   inverse B (thread (k1, n3)): * conj W128^{n3 k2}, DFT16 over k2
+//   inverse C (thread m): * conj W2048^{m k1}, DFT16 over k1 -> z[m + 128 n1] -> sink
+// then the polyphase FIR of each beam (fir_polyphase, all 256 threads).
+// ---------------------------------------------------------------------------
+constexpr int kP2M = 2048, kP2Buf = kP2M + kP2M / 8; // complex slots per beam (pad8)
+// one pad slot per 8 complex: the middle pass's 8-element rows 128 k1 + 8 k2
+// land at 144 k1 + 9 k2, distinct 16-byte bank groups for the 8 consecutive
+// k2 of a quarter-warp; the passes' runs of 8 consecutive positions stay
+// conflict-free
+__device__ __forceinline__ int pad8(int i) { return i + (i >> 3); }
+
+template <typename V, typename TW>
+__device__ __forceinline__ void tw_powers_m(const TW& tw, int M, int ns, int k, V (&w)[16]) {
+    w[1] = tw.w(M, ns, 16, k, 1);
+    w[2] = tw.w(M, ns, 16, k, 2);
+    w[4] = tw.w(M, ns, 16, k, 4);
+    w[8] = tw.w(M, ns, 16, k, 8);
+    w[3] = cmul(w[1], w[2]);
+    w[5] = cmul(w[1], w[4]);
+    w[6] = cmul(w[2], w[4]);
+    w[7] = cmul(w[3], w[4]);
+#pragma unroll
+    for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kThreads, SNB_ENV_MINB) k_envelope_pair2048(EnvArgs a, FirTaps<R> taps) {
+    using V = typename Cx<R>::T;
+    constexpr int M = kP2M, N = 2 * M;
+    extern __shared__ __align__(16) unsigned char smem[];
+    R* comp = reinterpret_cast<R*>(smem);
+    V* buf0 = reinterpret_cast<V*>(comp + kFirTaps);
+    const int t = threadIdx.x, h = t >> 7, u = t & 127;
+    V* buf = buf0 + h * kP2Buf;
+    for (int i = t; i < kFirTaps; i += blockDim.x) comp[i] = taps.c[i];
+    __syncthreads();
+    const TwGlobal<V> tw{reinterpret_cast<const V*>(a.tw), 2};
+    const int64_t items = a.n_dirs * a.batch, pairs = (items + 1) / 2;
+    const R s = (R)2 / (R)N;
+    const int c0 = (a.comp_len - 1) / 2, D = a.decim, PL = a.phase_len;
+    const int Li = (int)a.mf_len;
+    auto cosS = [](int S) { return (R)(S <= 8 ? cos_pi16(S) : -cos_pi16(16 - S)); };
+    auto sinS = [](int S) { return (R)cos_pi16(S <= 8 ? 8 - S : S - 8); };
+    for (int64_t p = blockIdx.x; p < pairs; p += gridDim.x) {
+        const int64_t it = 2 * p + h;
+        const bool live = it < items;
+        const int64_t src_it = live ? it : items - 1; // the idle half recomputes a beam (barriers)
+        const V* src = reinterpret_cast<const V*>(a.beams) + (size_t)src_it * M;
+        {
+            const int64_t nx = 2 * (p + gridDim.x) + h;
+            if (nx < items && u == 0) {
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const V*>(a.beams) + (size_t)nx * M),
+                             "r"((unsigned)(M * sizeof(V))) : "memory");
+            }
+        }
+        {   // forward pass 1
+            V v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = __ldg(src + u + 128 * r);
+            dft16<false>(v);
+            V w[16];
+            tw_powers_m(tw, M, 128, u, w);
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const int k1 = out_slot<16>(r);
+                buf[pad8(u + 128 * k1)] = k1 ? cmul(v[r], w[k1 ? k1 : 1]) : v[r];
+            }
+        }
+        __syncthreads();
+        {   // forward pass 2
+            const int k1 = u >> 3, n3 = u & 7;
+            V v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = buf[pad8(128 * k1 + 8 * r + n3)];
+            dft16<false>(v);
+            V w[16];
+            tw_powers_m(tw, M, 8, n3, w);
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const int k2 = out_slot<16>(r);
+                buf[pad8(128 * k1 + 8 * k2 + n3)] = k2 ? cmul(v[r], w[k2 ? k2 : 1]) : v[r];
+            }
+        }
+        __syncthreads();
+        {   // middle: DFT8, Hilbert operator, inverse DFT8 (thread-local rows)
+            // rows: u = 8 c + d -> ra = c + 16 d (k1 = c fixed, k2 = d spread
+            // over a quarter-warp), rb = 256 - ra (u = 0: rows 0 and 128)
+            const int ra = (u >> 3) + 16 * (u & 7), rb = u == 0 ? 128 : 256 - ra;
+            const int ba = 128 * (ra & 15) + 8 * (ra >> 4), bb = 128 * (rb & 15) + 8 * (rb >> 4);
+            V xa[8], xb[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                xa[r] = buf[pad8(ba + r)];
+                xb[r] = buf[pad8(bb + r)];
+            }
+            dft8<false>(xa);
+            dft8<false>(xb);
+            // op(zk, zc, c, sn) = s (cos t conj(zc) + i sin t zk), c = s cos t, sn = s sin t
+            auto op = [](V zk, V zc, R c, R sn) { return V{c * zc.x - sn * zk.y, sn * zk.x - c * zc.y}; };
+            V na[8], nb[8];
+            const V ha = tw.h(ra), hb = tw.h(rb);
+            const R cja = s * ha.x, sja = -s * ha.y, cjb = s * hb.x, sjb = -s * hb.y;
+            if (u != 0) {
+                // bin ra + 256 k3 <-> rb + 256 (7 - k3), angle of the partner = pi - t
+#pragma unroll
+                for (int k3 = 0; k3 < 8; ++k3) {
+                    const R c = cja * cosS(2 * k3) - sja * sinS(2 * k3);
+                    const R sn = sja * cosS(2 * k3) + cja * sinS(2 * k3);
+                    na[k3] = op(xa[k3], xb[7 - k3], c, sn);
+                    nb[7 - k3] = op(xb[7 - k3], xa[k3], -c, sn);
+                }
+            } else {
+                // row 0: bins 256 k3 <-> 256 (8 - k3) (k3 = 4 with itself), DC
+                // and Nyquist (Z[0]) zeroed; row 128: k3 <-> 7 - k3
+                na[0] = V{(R)0, (R)0};
+#pragma unroll
+                for (int k3 = 1; k3 < 8; ++k3) na[k3] = op(xa[k3], xa[8 - k3], s * cosS(2 * k3), s * sinS(2 * k3));
+#pragma unroll
+                for (int k3 = 0; k3 < 8; ++k3) {
+                    const R c = cjb * cosS(2 * k3) - sjb * sinS(2 * k3);
+                    const R sn = sjb * cosS(2 * k3) + cjb * sinS(2 * k3);
+                    nb[k3] = op(xb[k3], xb[7 - k3], c, sn);
+                }
+            }
+            dft8<true>(na);
+            dft8<true>(nb);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                buf[pad8(ba + r)] = na[r];
+                buf[pad8(bb + r)] = nb[r];
+            }
+        }
+        __syncthreads();
+        {   // inverse B
+            const int k1 = u >> 3, n3 = u & 7;
+            V v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = buf[pad8(128 * k1 + 8 * r + n3)];
+            V w[16];
+            tw_powers_m(tw, M, 8, n3, w);
+#pragma unroll
+            for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], cconj(w[r]));
+            dft16<true>(v);
+#pragma unroll
+            for (int r = 0; r < 16; ++r) buf[pad8(128 * k1 + 8 * out_slot<16>(r) + n3)] = v[r];
+        }
+        __syncthreads();
+        {   // inverse C + sink: |b + iH(b)| into the decimation-phase rows of this beam
+            V v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = buf[pad8(128 * r + u)];
+            V w[16];
+            tw_powers_m(tw, M, 128, u, w);
+#pragma unroll
+            for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], cconj(w[r]));
+            dft16<true>(v);
+            __syncthreads();
+            R* ph = reinterpret_cast<R*>(buf);
+            const unsigned dmagic = 0xffffffffu / (unsigned)D + 1u;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const int n = u + 128 * out_slot<16>(r);
+                const V hv = v[r];
+                const V bv = __ldg(src + n);
+                const R m0 = fast_sqrt(bv.x * bv.x + hv.x * hv.x);
+                const R m1 = fast_sqrt(bv.y * bv.y + hv.y * hv.y);
+                const unsigned tt = 2u * (unsigned)n + (unsigned)c0;
+                const int uu = (int)__umulhi(tt, dmagic);
+                const int pp = (int)tt - uu * D;
+                if (2 * n < Li) ph[pp * PL + uu] = m0;
+                if (2 * n + 1 < Li) ph[pp + 1 == D ? uu + 1 : (pp + 1) * PL + uu] = m1;
+            }
+            if (u < D) {
+                const int pr = u;
+                const int lo = c0 >= pr ? (c0 - pr + D - 1) / D : 0;
+                const int hi = (int)((a.mf_len + c0 - pr + D - 1) / D);
+                R* row = ph + pr * PL;
+                for (int k = 0; k < lo; ++k) row[k] = 0;
+                for (int k = hi; k < PL; ++k) row[k] = 0;
+            }
+        }
+        __syncthreads();
+        {
+            // polyphase FIR of this half's beam over its 4 warps: units (output
+            // group, phase half) with the half warp-uniform (warps 0, 2: phases
+            // 0-4; 1, 3: 5-9), 64 groups per round; the upper half's partial
+            // sums through shared memory after the phase rows
+            const R* ph = reinterpret_cast<const R*>(buf);
+            R* red = reinterpret_cast<R*>(buf) + D * PL;
+            const int groups = (int)((a.bins + kFirR - 1) / kFirR);
+            const int wl = u >> 5, q = wl & 1, gl = (wl >> 1) * 32 + (u & 31);
+            const int64_t b = src_it / a.n_dirs, slot = src_it % a.n_dirs;
+            float* eo = a.energy + ((size_t)b * a.n_dirs + a.order[slot]) * a.bins;
+#pragma unroll 1
+            for (int g0 = 0; g0 < groups; g0 += 64) {
+                const int g = g0 + gl, k0 = g * kFirR;
+                R acc[kFirR];
+#pragma unroll
+                for (int r = 0; r < kFirR; ++r) acc[r] = 0;
+                if (g < groups) {
+                    if (q == 0) fir_phases<0, kFirD / 2>(ph, PL, k0, acc, comp);
+                    else fir_phases<kFirD / 2, kFirD / 2>(ph, PL, k0, acc, comp);
+                    if (q) {
+#pragma unroll
+                        for (int r = 0; r < kFirR; ++r) red[gl * kFirR + r] = acc[r];
+                    }
+                }
+                __syncthreads();
+                if (live && g < groups && q == 0) {
+#pragma unroll
+                    for (int r = 0; r < kFirR; ++r) {
+                        if (k0 + r < a.bins) {
+                            const float v = (float)(acc[r] + red[gl * kFirR + r]);
+                            eo[k0 + r] = v > 0.0f ? v : 0.0f;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_envelope_split8192: the envelope for N = 16384 (M = 8192; the 8-11.7 m
+// windows). One radix-2 DIF stage splits the 8192-point transform into its
+// even- and odd-bin 4096-point halves, each run by one 256-thread half of the
+// CTA with the in-place M = 4096 passes (dif_pass1/2, the Hilbert middle pass
+// -- the even half's pairing and angles are exactly the M = 4096 ones, the
+// odd half pairs k' with 4095 - k' -- and dit_pass2/3); the inverse radix-2
+// stage recombines z'[n] = e'[n] +- W8192^{-n} o'[n] and feeds the sink. The
+// polyphase FIR then runs over all 512 threads (units of output group x
+// phase part). Replaces the generic Stockham path (two butterflies per thread
+// per pass, 241 registers, 8 warps per SM).
+// ---------------------------------------------------------------------------
+constexpr int kS8Buf = 4096 + 256; // complex slots per half (pad16)
+
+template <typename R>
+__global__ void __launch_bounds__(2 * kThreads, 1) k_envelope_split8192(EnvArgs a, FirTaps<R> taps) {
+    using V = typename Cx<R>::T;
+    constexpr int M = 8192, N = 2 * M;
+    extern __shared__ __align__(16) unsigned char smem[];
+    V* tws = reinterpret_cast<V*>(smem);
+    R* comp = reinterpret_cast<R*>(tws + kTwSharedCount);
+    V* buf0 = reinterpret_cast<V*>(comp + kFirTaps);
+    for (int i = threadIdx.x; i < kTwSharedCount; i += blockDim.x) tws[i] = reinterpret_cast<const V*>(a.tw_small)[i];
+    for (int i = threadIdx.x; i < kFirTaps; i += blockDim.x) comp[i] = taps.c[i];
+    __syncthreads();
+    const TwShared<V> tw4{tws};
+    const V* tw = reinterpret_cast<const V*>(a.tw); // e^{-2 pi i k / 16384}
+    const int64_t items = a.n_dirs * a.batch;
+    const R s = (R)2 / (R)N;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        // per-item thread indices, opaque to the compiler: loop-invariant
+        // addresses hoisted out of the item loop would not fit the registers
+        int t = threadIdx.x;
+        asm volatile("" : "+r"(t));
+        const int h = t >> 8, j = t & 255;
+        V* buf = buf0 + h * kS8Buf;
+        const int c0 = (a.comp_len - 1) / 2, D = a.decim, PL = a.phase_len;
+        const int Li = (int)a.mf_len;
+        const V* src = reinterpret_cast<const V*>(a.beams) + (size_t)it * M;
+        {
+            const int64_t nx = it + gridDim.x;
+            if (nx < items && t == 0) {
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const V*>(a.beams) + (size_t)nx * M),
+                             "r"((unsigned)(M * sizeof(V))) : "memory");
+            }
+        }
+        {   // radix-2 DIF stage: e[n] = z[n] + z[n + 4096], o[n] = (z[n] - z[n + 4096]) W8192^n
+            V v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const int n = j + 256 * r;
+                const V z0 = __ldg(src + n), z1 = __ldg(src + n + 4096);
+                v[r] = h == 0 ? cadd(z0, z1) : cmul(csub(z0, z1), __ldg(tw + 2 * n));
+            }
+            dif_pass1_4096(v, buf, tw4);
+        }
+        dif_pass2_4096(buf, tw4);
+        if (h == 0) hilbert_mid_dif_4096(buf, tw4, s);
+        else hilbert_mid_dif_4096_odd(buf, tw4, tw, s);
+        dit_pass2_4096(buf, tw4);
+        dit_pass3_4096(buf, tw4, [&](int n, V v) { buf[pad16(n)] = v; });
+        __syncthreads();
+        // inverse radix-2 stage + sink: z'[n + 4096 h] = e'[n] +- conj(W8192^n) o'[n]
+        V zz[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int n = j + 256 * r;
+            const V e = buf0[pad16(n)];
+            const V o = cmul(buf0[kS8Buf + pad16(n)], cconj(__ldg(tw + 2 * n)));
+            zz[r] = h == 0 ? cadd(e, o) : csub(e, o);
+        }
+        __syncthreads();
+        {
+            R* ph = reinterpret_cast<R*>(buf0);
+            const unsigned dmagic = 0xffffffffu / (unsigned)D + 1u;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const int n = j + 256 * r + 4096 * h;
+                const V hv = zz[r];
+                const V bv = __ldg(src + n);
+                const R m0 = fast_sqrt(bv.x * bv.x + hv.x * hv.x);
+                const R m1 = fast_sqrt(bv.y * bv.y + hv.y * hv.y);
+                const unsigned tt = 2u * (unsigned)n + (unsigned)c0;
+                const int uu = (int)__umulhi(tt, dmagic);
+                const int pp = (int)tt - uu * D;
+                if (2 * n < Li) ph[pp * PL + uu] = m0;
+                if (2 * n + 1 < Li) ph[pp + 1 == D ? uu + 1 : (pp + 1) * PL + uu] = m1;
+            }
+            if (t < D) {
+                const int pr = t;
+                const int lo = c0 >= pr ? (c0 - pr + D - 1) / D : 0;
+                const int hi = (int)((a.mf_len + c0 - pr + D - 1) / D);
+                R* row = ph + pr * PL;
+                for (int k = 0; k < lo; ++k) row[k] = 0;
+                for (int k = hi; k < PL; ++k) row[k] = 0;
+            }
+        }
+        __syncthreads();
+        {
+            // polyphase FIR: units (output group, phase part), the part
+            // warp-uniform (warp w: part w mod 4 of 3 + 3 + 2 + 2 phases), 128
+            // groups per round; partial sums of parts 1-3 through shared
+            // memory after the phase rows
+            const R* ph = reinterpret_cast<const R*>(buf0);
+            R* red = reinterpret_cast<R*>(buf0) + D * PL;
+            const int groups = (int)((a.bins + kFirR - 1) / kFirR);
+            const int q = (t >> 5) & 3, gl = (t >> 7) * 32 + (t & 31);
+            const int64_t b = it / a.n_dirs, slot = it % a.n_dirs;
+            float* eo = a.energy + ((size_t)b * a.n_dirs + a.order[slot]) * a.bins;
+#pragma unroll 1
+            for (int g0 = 0; g0 < groups; g0 += 128) {
+                const int g = g0 + gl, k0 = g * kFirR;
+                R acc[kFirR];
+#pragma unroll
+                for (int r = 0; r < kFirR; ++r) acc[r] = 0;
+                if (g < groups) {
+                    if (q == 0) fir_phases<0, 3>(ph, PL, k0, acc, comp);
+                    else if (q == 1) fir_phases<3, 3>(ph, PL, k0, acc, comp);
+                    else if (q == 2) fir_phases<6, 2>(ph, PL, k0, acc, comp);
+                    else fir_phases<8, 2>(ph, PL, k0, acc, comp);
+                    if (q) {
+#pragma unroll
+                        for (int r = 0; r < kFirR; ++r) red[((q - 1) * 128 + gl) * kFirR + r] = acc[r];
+                    }
+                }
+                __syncthreads();
+                if (g < groups && q == 0) {
+#pragma unroll
+                    for (int r = 0; r < kFirR; ++r) {
+                        if (k0 + r < a.bins) {
+                            const R sum = acc[r] + red[gl * kFirR + r] + red[(128 + gl) * kFirR + r] +
+                                          red[(256 + gl) * kFirR + r];
+                            const float v = (float)sum;
+                            eo[k0 + r] = v > 0.0f ? v : 0.0f;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+}
+
+size_t envelope_split8192_smem_bytes(bool f32) {
+    const size_t rb = f32 ? 4 : 8;
+    return (size_t)kTwSharedCount * 2 * rb + (size_t)kFirTaps * rb + (size_t)2 * kS8Buf * 2 * rb;
+}
+
+int envelope_split8192_blocks_per_sm(bool f32) {
+    int n = 0;
+    const size_t smem = envelope_split8192_smem_bytes(f32);
+    if (f32) {
+        set_smem((const void*)k_envelope_split8192<float>, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_envelope_split8192<float>, 2 * kThreads, smem);
+    } else {
+        set_smem((const void*)k_envelope_split8192<double>, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_envelope_split8192<double>, 2 * kThreads, smem);
+    }
+    return n;
+}
+
+size_t envelope_pair2048_smem_bytes(bool f32) {
+    const size_t rb = f32 ? 4 : 8;
+    return (size_t)kFirTaps * rb + (size_t)2 * kP2Buf * 2 * rb;
 }
 
 // Workspace::beamform accessor (pipeline.cpp:576-591): materialised beams
@@ -897,18 +1298,53 @@ static void env_ff_launch(const EnvArgs& a, const FirTaps<R>& taps, int grid, cu
     k_envelope<R, kFfGroups, 4096, true><<<grid, kThreads * kFfGroups, smem, s>>>(a, taps);
 }
 
+int envelope_pair2048_blocks_per_sm(bool f32) {
+    int n = 0;
+    const size_t smem = envelope_pair2048_smem_bytes(f32);
+    if (f32) {
+        set_smem((const void*)k_envelope_pair2048<float>, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_envelope_pair2048<float>, kThreads, smem);
+    } else {
+        set_smem((const void*)k_envelope_pair2048<double>, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_envelope_pair2048<double>, kThreads, smem);
+    }
+    return n;
+}
+
 void launch_envelope(const EnvArgs& a, const FirTaps<float>& t32, const FirTaps<double>& t64, bool f32,
                      int grid, cudaStream_t s) {
+    if (a.split8192) {
+        const size_t smem = envelope_split8192_smem_bytes(f32);
+        if (f32) {
+            set_smem((const void*)k_envelope_split8192<float>, smem);
+            k_envelope_split8192<float><<<grid, 2 * kThreads, smem, s>>>(a, t32);
+        } else {
+            set_smem((const void*)k_envelope_split8192<double>, smem);
+            k_envelope_split8192<double><<<grid, 2 * kThreads, smem, s>>>(a, t64);
+        }
+        return;
+    }
+    if (a.pair2048) {
+        const size_t smem = envelope_pair2048_smem_bytes(f32);
+        if (f32) {
+            set_smem((const void*)k_envelope_pair2048<float>, smem);
+            k_envelope_pair2048<float><<<grid, kThreads, smem, s>>>(a, t32);
+        } else {
+            set_smem((const void*)k_envelope_pair2048<double>, smem);
+            k_envelope_pair2048<double><<<grid, kThreads, smem, s>>>(a, t64);
+        }
+        return;
+    }
     if (a.fir_fft) {
         if (f32) env_ff_launch<float>(a, t32, grid, s);
         else env_ff_launch<double>(a, t64, grid, s);
         return;
     }
     if (f32) {
-        const size_t smem = envelope_smem_bytes(a.n, a.fir_q * a.decim, a.decim * a.phase_len, true, kEnvGroupsF32);
+        const size_t smem = envelope_smem_bytes(a.n, a.fir_fast ? kFirTaps : a.fir_q * a.decim, a.decim * a.phase_len, true, kEnvGroupsF32);
         SNB_DISPATCH_M(a.n / 2, (env_launch<float, kEnvGroupsF32, MM>(a, t32, grid, smem, s)))
     } else {
-        const size_t smem = envelope_smem_bytes(a.n, a.fir_q * a.decim, a.decim * a.phase_len, false, kEnvGroupsF64);
+        const size_t smem = envelope_smem_bytes(a.n, a.fir_fast ? kFirTaps : a.fir_q * a.decim, a.decim * a.phase_len, false, kEnvGroupsF64);
         SNB_DISPATCH_M(a.n / 2, (env_launch<double, kEnvGroupsF64, MM>(a, t64, grid, smem, s)))
     }
 }

@@ -78,6 +78,8 @@ struct EnvArgs {
     int fir_fft;             // FIR by 768-point FFTs (fir_fft768, fft.cuh): N == 8192 and the shapes fit
     const void* ff_u;        // [16][240] spectrum factors U_a in register order (double2 or float2)
     const void* ff_w;        // e^{-2 pi i e / 768}, e < 768
+    int pair2048;            // N = 4096 with the fast FIR: k_envelope_pair2048 (two beams per group)
+    int split8192;           // N = 16384 with the fast FIR: k_envelope_split8192 (radix-2 + two 4096 halves)
 };
 
 // Polyphase smoothing FIR fast path (the reference's default composite
@@ -109,6 +111,10 @@ size_t envelope_ff_smem_bytes(bool f32);
 int envelope_ff_blocks_per_sm(bool f32); // 0: does not fit
 __host__ __device__ int envelope_group_reals(int n, int phase_reals);
 int envelope_blocks_per_sm(bool f32, int n_fft, size_t smem);
+size_t envelope_pair2048_smem_bytes(bool f32);
+int envelope_pair2048_blocks_per_sm(bool f32); // 0: does not fit
+size_t envelope_split8192_smem_bytes(bool f32);
+int envelope_split8192_blocks_per_sm(bool f32); // 0: does not fit
 void launch_rfft_forward(const double* x, double2* X, const double2* tw, int n, size_t smem,
                          cudaStream_t s);
 

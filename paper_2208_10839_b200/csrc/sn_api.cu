@@ -186,7 +186,7 @@ struct sn_workspace {
     DemodArgs demod{};
     int demod_grid = 0;
     size_t demod_smem = 0, mf_smem = 0, dir_smem = 0;
-    int dir_grid = 0, halo = 0, tile = 0, fir_q = 0, phase_len = 0, fir_fast = 0;
+    int dir_grid = 0, halo = 0, tile = 0, fir_q = 0, phase_len = 0, fir_fast = 0, pair2048 = 0, split8192 = 0;
     // wire-format frames (frames.cu)
     uint32_t* d_crc_slice = nullptr;
     uint32_t* d_crc_shift = nullptr;
@@ -472,11 +472,29 @@ struct sn_workspace {
                 }
             }
         }
-        dir_smem = envelope_smem_bytes((int)s.env_fft, fir_q * plan.cfg.post_envelope_decimation,
+        dir_smem = envelope_smem_bytes((int)s.env_fft,
+                                       fir_fast ? kFirTaps : fir_q * plan.cfg.post_envelope_decimation,
                                        plan.cfg.post_envelope_decimation * phase_len, f32,
                                        f32 ? kEnvGroupsF32 : kEnvGroupsF64);
         {
             dir_grid = sms * envelope_blocks_per_sm(f32, (int)s.env_fft, dir_smem);
+            // N = 4096 (the 1.5 m window): two beams per group, when the phase
+            // rows + FIR scratch of a beam fit its FFT buffer
+            pair2048 = s.env_fft == 4096 && fir_fast &&
+                       plan.cfg.post_envelope_decimation * phase_len + 64 * kFirR <= 2 * (2048 + 256);
+            if (pair2048) {
+                const int per = envelope_pair2048_blocks_per_sm(f32);
+                if (per > 0) dir_grid = sms * per;
+                else pair2048 = 0;
+            }
+            // N = 16384 (8-11.7 m): radix-2 split into two M = 4096 halves
+            split8192 = s.env_fft == 16384 && fir_fast &&
+                        plan.cfg.post_envelope_decimation * phase_len + 3 * 128 * kFirR <= 2 * 2 * (4096 + 256);
+            if (split8192) {
+                const int per = envelope_split8192_blocks_per_sm(f32);
+                if (per > 0) dir_grid = sms * per;
+                else split8192 = 0;
+            }
             if (fir_fft) {
                 const int per = envelope_ff_blocks_per_sm(f32);
                 if (per > 0) dir_grid = sms * per;
@@ -785,6 +803,8 @@ struct sn_workspace {
         ea.phase_len = phase_len;
         ea.fir_fast = fir_fast;
         ea.fir_fft = fir_fft;
+        ea.pair2048 = pair2048;
+        ea.split8192 = split8192;
         ea.ff_u = f32 ? (const void*)d_ff_u32 : (const void*)d_ff_u;
         ea.ff_w = f32 ? (const void*)d_ff_w32 : (const void*)d_ff_w;
         launch_envelope(ea, taps32, taps64, f32, dir_grid, s);
