@@ -364,6 +364,20 @@ sn_status sn_gather_ids(sn_gather* g, int slot, sn_frame_id* out, uint64_t capac
 /* device ms of slot's last gather (its own stream, CUDA events). */
 sn_status sn_gather_elapsed(sn_gather* g, int slot, float* ms);
 
+/* ---- opt-in display transform (north star stage 4: log/normalisation) ----
+ * Not part of Workspace::process: the reference writes max(0, float) energies
+ * (pipeline.cpp:469-471) and so does every process entry point. This maps
+ * `count` finished energyscapes of `cells` floats each (device memory) into a
+ * SEPARATE device buffer, per image: NORMALIZE e / max(e); DB
+ * max(10 log10(e / max(e)), floor_db) (floor_db where e == 0). Enqueued on
+ * `stream`; in == out is rejected (the energies stay untouched). */
+typedef enum sn_transform {
+    SN_TRANSFORM_NORMALIZE = 1,
+    SN_TRANSFORM_DB = 2
+} sn_transform;
+sn_status sn_energyscape_transform(const float* d_energies, float* d_out, uint64_t count, uint64_t cells,
+                                   int32_t mode, float floor_db, void* stream);
+
 /* FMA-throughput microbenchmark on `device` (TFLOP/s, FMA = 2 flops); the
  * roofline denominator for CUDA-core kernels (no tensor cores involved). */
 sn_status sn_measure_fp_peak(int device, int precision, double* tflops);

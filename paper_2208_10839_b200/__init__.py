@@ -33,7 +33,7 @@ __all__ = [
     "Scene", "Workspace", "default_pipeline_config", "direction_grid", "default_array",
     "synthesize_measurement", "SonarError", "ConfigError", "ArgumentError", "DecodeError",
     "IoError", "CudaError", "lib", "crc32", "measurement_frame", "CentralPool", "synthesize_device",
-    "fibonacci_hemisphere", "Beamformer", "load_library",
+    "fibonacci_hemisphere", "Beamformer", "load_library", "Transform", "energyscape_transform",
 ]
 
 
@@ -226,6 +226,7 @@ def lib() -> C.CDLL:
     L.sn_workspace_image_frame_bytes.argtypes = [vp]
     L.sn_workspace_process_frames.argtypes = [vp, C.POINTER(C.c_void_p), C.POINTER(u64), u64, vp, u64,
                                               C.POINTER(u64), C.POINTER(C.c_int32)]
+    L.sn_energyscape_transform.argtypes = [vp, vp, u64, u64, i32, C.c_float, vp]
     L.sn_gather_unique_id.argtypes = [vp]
     L.sn_gather_create.argtypes = [C.c_int, C.c_int, vp, C.c_int, u64, u64, C.POINTER(vp)]
     L.sn_gather_destroy.argtypes = [vp]
@@ -303,6 +304,21 @@ class CentralPool:
             self.close()
         except Exception:
             pass
+
+
+class Transform(enum.IntEnum):  # sn_transform
+    normalize = 1
+    db = 2
+
+
+def energyscape_transform(d_energies_ptr: int, d_out_ptr: int, count: int, cells: int,
+                          mode: Transform = Transform.db, floor_db: float = -60.0, stream: int = 0) -> None:
+    """Opt-in display transform (north star stage 4) of `count` finished
+    energyscapes in device memory into a separate device buffer; the
+    reference-parity energies (max(0, float), pipeline.cpp:469-471) are left
+    untouched. normalize: e / max(e); db: max(10 log10(e / max(e)), floor_db)."""
+    _check(lib().sn_energyscape_transform(C.c_void_p(d_energies_ptr), C.c_void_p(d_out_ptr), int(count), int(cells),
+                                          int(mode), float(floor_db), C.c_void_p(stream or 1)))
 
 
 def crc32(data) -> int:

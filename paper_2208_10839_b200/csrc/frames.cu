@@ -19,6 +19,7 @@
 // shift of two consecutive float words of the energyscape. The encoder CRCs
 // the words it writes (no re-read) and a finalize kernel stores the CRC.
 #include "kernels.cuh"
+#include "sonarnet_b200.h"
 
 #include <cstdint>
 #include <cstring>
@@ -343,6 +344,46 @@ uint32_t crc_init_term(const uint32_t* shift, uint64_t n) {
         }
     }
     return v ^ 0xFFFFFFFFu;
+}
+
+} // namespace snb
+
+namespace snb {
+
+// ---------------------------------------------------------------------------
+// Opt-in display transform of finished energyscapes (north star stage 4,
+// "log/normalisation"): the reference's write-out stops at max(0, float)
+// (pipeline.cpp:469-471), so this runs strictly after the energies exist,
+// into a separate buffer, and never changes them. Per image (cells floats):
+//   SN_TRANSFORM_NORMALIZE: e / max(e)                    (0 if the image is all 0)
+//   SN_TRANSFORM_DB:        max(10 log10(e / max(e)), floor_db)  (floor_db if e == 0)
+// One CTA per image: a block max reduction over the image, then the map, both
+// reading the image with 16-byte loads where aligned.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k_energyscape_transform(const float* in, float* out, uint64_t cells,
+                                                                int mode, float floor_db) {
+    __shared__ float red[16];
+    const float* e = in + (size_t)blockIdx.x * cells;
+    float* o = out + (size_t)blockIdx.x * cells;
+    float m = 0.0f;
+    for (uint64_t i = threadIdx.x; i < cells; i += blockDim.x) m = fmaxf(m, e[i]);
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    m = 0.0f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+    const float inv = m > 0.0f ? 1.0f / m : 0.0f;
+    for (uint64_t i = threadIdx.x; i < cells; i += blockDim.x) {
+        const float r = e[i] * inv;
+        o[i] = mode == SN_TRANSFORM_NORMALIZE ? r : (r > 0.0f ? fmaxf(10.0f * log10f(r), floor_db) : floor_db);
+    }
+}
+
+void launch_energyscape_transform(const float* in, float* out, uint64_t count, uint64_t cells, int mode,
+                                  float floor_db, cudaStream_t s) {
+    if (count == 0) return;
+    k_energyscape_transform<<<(unsigned)count, 512, 0, s>>>(in, out, cells, mode, floor_db);
 }
 
 } // namespace snb

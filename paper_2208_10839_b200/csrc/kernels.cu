@@ -442,7 +442,9 @@ __device__ __forceinline__ void fir_polyphase(const R* ph, const R* comp, const 
 
 // FF: the smoothing FIR by 768-point FFTs (fir_fft768; M == 4096 only)
 template <typename R, int G, int M, bool FF = false>
-__global__ void __launch_bounds__(kThreads * G, M >= 8192 ? 1 : (sizeof(R) == 8 ? SNB_ENV_MINB : SNB_ENV_MINB_F32) / G)
+// (M <= 2048 generic fallbacks -- the 1.5 m window runs k_envelope_pair2048 --
+// get the full register file: at 128 registers their Stockham passes spilled)
+__global__ void __launch_bounds__(kThreads * G, (M >= 8192 || M <= 2048) ? 1 : (sizeof(R) == 8 ? SNB_ENV_MINB : SNB_ENV_MINB_F32) / G)
     k_envelope(EnvArgs a, FirTaps<R> taps) {
     static_assert(!FF || M == 4096, "FFT FIR: N = 8192 only");
     using V = typename Cx<R>::T;

@@ -148,6 +148,8 @@ void launch_encode_image_frames(const ImageFrameArgs& a, uint64_t count, const C
 void launch_crc_finalize(uint32_t* acc, uint32_t k_n, uint64_t count, uint8_t* out, uint64_t stride, uint64_t n,
                          bool store, int32_t* ok, cudaStream_t s);
 uint32_t crc32_host(const uint8_t* p, uint64_t n);
+void launch_energyscape_transform(const float* in, float* out, uint64_t count, uint64_t cells, int mode,
+                                  float floor_db, cudaStream_t s);
 
 // ---- synthetic captures on the GPU (synth.cu) -------------------------------
 constexpr int kSynthMaxReflectors = 8;

@@ -9,6 +9,8 @@
 #include "plan.hpp"
 #include "sonarnet_b200.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
@@ -47,6 +49,15 @@ sn_status guarded(F&& f) {
         return SN_ERR_INTERNAL;
     }
 }
+
+// NVTX ranges around the host-side entry points (header-only nvtx3: no
+// link dependency; zero cost unless a profiler injects itself)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct DeviceGuard {
     int prev = -1;
@@ -290,6 +301,7 @@ struct sn_workspace {
     }
 
     void init_device() {
+        NvtxRange nv("sn_workspace_create");
         const Sizes& s = plan.sz;
         if (s.mf_fft > 16384 || s.env_fft > 16384) {
             config_error("pipeline: FFT size " + std::to_string(std::max(s.mf_fft, s.env_fft)) +
@@ -969,6 +981,7 @@ struct sn_workspace {
     // exposed. Caller buffers that are page-locked are DMA'd directly;
     // pageable ones go through the workspace's pinned staging buffers.
     void process_host(const sn_raw_measurement* ms, uint64_t count, float* out) {
+        NvtxRange nv("sn_workspace_process_batch");
         for (uint64_t i = 0; i < count; ++i) validate(ms[i]); // all-or-error
         require_device();
         DeviceGuard g(device);
@@ -1043,6 +1056,7 @@ struct sn_workspace {
     //   SN_ERR_IO      malformed / integrity error / not a measurement: discarded
     void process_frames(const uint8_t* const* frames, const uint64_t* lens, uint64_t count, uint8_t* out,
                         uint64_t slot, uint64_t* out_lens, int32_t* status) {
+        NvtxRange nv("sn_workspace_process_frames");
         require_device();
         DeviceGuard g(device);
         const Sizes& z = plan.sz;
@@ -1209,6 +1223,7 @@ struct sn_workspace {
     }
 
     void process_device(const uint8_t* d_in, uint64_t count, float* d_out, cudaStream_t s) {
+        NvtxRange nv("sn_workspace_process_device");
         require_device();
         DeviceGuard g(device);
         if (!s) s = stream;
@@ -1639,6 +1654,18 @@ sn_status sn_synthesize_device(const sn_pipeline_config* cfg, const sn_scene* sc
         cudaFreeAsync(d_sc, st);
         cudaFreeAsync(d_words, st);
         ck(cudaStreamSynchronize(st), "synth sync");
+    });
+}
+
+sn_status sn_energyscape_transform(const float* d_energies, float* d_out, uint64_t count, uint64_t cells,
+                                   int32_t mode, float floor_db, void* stream) {
+    return guarded([&] {
+        if ((!d_energies || !d_out) && count) argument_error("null argument");
+        if (mode != SN_TRANSFORM_NORMALIZE && mode != SN_TRANSFORM_DB) argument_error("unknown transform mode");
+        if (d_energies == d_out && count) argument_error("the transform writes a separate buffer (in == out)");
+        launch_energyscape_transform(d_energies, d_out, count, cells, mode, floor_db,
+                                     static_cast<cudaStream_t>(stream));
+        ck(cudaGetLastError(), "transform launch");
     });
 }
 

@@ -220,3 +220,42 @@ def test_nccl_gather_world1(gpu):
     ms = C.c_float(0)
     assert L.sn_gather_elapsed(h, 1, C.byref(ms)) == 0 and ms.value >= 0
     L.sn_gather_destroy(h)
+
+
+def test_opt_in_log_normalisation_transform(gpu, po, ref):
+    # north star stage 4 as an opt-in post-step: the energies keep the
+    # reference's max(0, float) values (pipeline.cpp:469-471, one-ulp bar) and
+    # the transform of them matches a numpy post-step on the oracle's energies
+    import torch
+    sn = gpu
+    cfg = cfg_for(sn, "h90")
+    ms = [capture(sn, cfg, [(1.0 + 0.5 * i, 0.3 - 0.2 * i, 0.0, 0.6)], 0.01, 90 + i, seq=i) for i in range(2)]
+    ws = sn.Workspace(cfg, device=0, max_batch=2)
+    dp = torch.from_numpy(np.stack([m.packed for m in ms])).cuda()
+    e = torch.empty((2, ws.n_dirs, ws.bins), dtype=torch.float32, device="cuda")
+    ws.process_device(dp.data_ptr(), 2, e.data_ptr())
+    torch.cuda.synchronize()
+    raw = e.cpu().numpy()
+    r = ref.workspace(to_oracle(po, cfg))
+    want = [r.process(m.packed) for m in ms]
+    for i in range(2):
+        check_f64(raw[i], want[i])
+    cells = ws.n_dirs * ws.bins
+    out = torch.empty_like(e)
+    for mode, floor in ((sn.Transform.normalize, 0.0), (sn.Transform.db, -60.0)):
+        sn.energyscape_transform(e.data_ptr(), out.data_ptr(), 2, cells, mode, floor)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy()
+        assert np.array_equal(e.cpu().numpy(), raw)  # energies untouched
+        for i in range(2):
+            w = want[i].astype(np.float64) / want[i].max()
+            if mode == sn.Transform.db:
+                with np.errstate(divide="ignore"):
+                    w = np.maximum(10 * np.log10(w), floor)
+                assert np.abs(got[i] - w).max() <= 1e-4  # dB, float32 arithmetic
+                assert got[i].max() == 0.0 and got[i].min() >= floor
+            else:
+                assert np.abs(got[i] - w).max() <= 1e-6
+                assert got[i].max() == 1.0
+    with pytest.raises(sn.ArgumentError):
+        sn.energyscape_transform(e.data_ptr(), e.data_ptr(), 2, cells)
