@@ -373,9 +373,8 @@ __global__ void __launch_bounds__(512) k_energyscape_transform(const float* in, 
     __syncthreads();
     m = 0.0f;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
-    const float inv = m > 0.0f ? 1.0f / m : 0.0f;
     for (uint64_t i = threadIdx.x; i < cells; i += blockDim.x) {
-        const float r = e[i] * inv;
+        const float r = m > 0.0f ? __fdiv_rn(e[i], m) : 0.0f; // the peak maps to exactly 1 (0 dB)
         o[i] = mode == SN_TRANSFORM_NORMALIZE ? r : (r > 0.0f ? fmaxf(10.0f * log10f(r), floor_db) : floor_db);
     }
 }
