@@ -226,14 +226,22 @@ def lib() -> C.CDLL:
     L.sn_workspace_image_frame_bytes.argtypes = [vp]
     L.sn_workspace_process_frames.argtypes = [vp, C.POINTER(C.c_void_p), C.POINTER(u64), u64, vp, u64,
                                               C.POINTER(u64), C.POINTER(C.c_int32)]
-    L.sn_energyscape_transform.argtypes = [vp, vp, u64, u64, i32, C.c_float, vp]
-    L.sn_gather_unique_id.argtypes = [vp]
-    L.sn_gather_create.argtypes = [C.c_int, C.c_int, vp, C.c_int, u64, u64, C.POINTER(vp)]
-    L.sn_gather_destroy.argtypes = [vp]
-    L.sn_gather_start.argtypes = [vp, C.c_int, vp, C.POINTER(FrameId), u64, vp, vp]
-    L.sn_gather_wait.argtypes = [vp, C.c_int, vp]
-    L.sn_gather_ids.argtypes = [vp, C.c_int, C.POINTER(FrameId), u64, C.POINTER(C.c_int32)]
-    L.sn_gather_elapsed.argtypes = [vp, C.c_int, C.POINTER(C.c_float)]
+    # (bound when present: load_library() may A/B an older build of the
+    # sources; the in-tree library exports every symbol of the header, which
+    # tests/test_host.py checks)
+    optional = {
+        "sn_energyscape_transform": [vp, vp, u64, u64, i32, C.c_float, vp],
+        "sn_gather_unique_id": [vp],
+        "sn_gather_create": [C.c_int, C.c_int, vp, C.c_int, u64, u64, C.POINTER(vp)],
+        "sn_gather_destroy": [vp],
+        "sn_gather_start": [vp, C.c_int, vp, C.POINTER(FrameId), u64, vp, vp],
+        "sn_gather_wait": [vp, C.c_int, vp],
+        "sn_gather_ids": [vp, C.c_int, C.POINTER(FrameId), u64, C.POINTER(C.c_int32)],
+        "sn_gather_elapsed": [vp, C.c_int, C.POINTER(C.c_float)],
+    }
+    for name, args in optional.items():
+        if hasattr(L, name):
+            getattr(L, name).argtypes = args
     _lib = L
     return L
 

@@ -1,6 +1,6 @@
 #!/bin/bash
 for n in "$@"; do
-  timeout 300 python bench.py --lib paper_2208_10839_b200/_lib/ab/lib$n.so --steps 20 --warmup 3 --no-cpu-baseline --latency-samples 5 --stream-frames 0 --precision f32 > gpurun_out/ab_$n.log 2>&1
+  timeout 300 python bench.py --lib paper_2208_10839_b200/_lib/ab/lib$n.so --steps 20 --warmup 3 --no-cpu-baseline --latency-samples 5 --no-sweep --stream-frames 0 --cpu-latency-calls 0 --stream-frames 0 --precision f32 > gpurun_out/ab_$n.log 2>&1
   python - "$n" <<'PY'
 import json,sys
 n=sys.argv[1]
