@@ -281,3 +281,35 @@ def test_trigger_synchronisation_check():
     ids = [(1, 100, 7), (1, 200, 8), (2, 100, 7), (2, 200, 8)]  # world 2, 2 images each
     assert triggers_synchronized(ids, 2)
     assert not triggers_synchronized([(1, 100, 7), (2, 100, 8)], 2)
+
+
+def test_hot_kernels_register_budget(sn):
+    # ptxas resource usage of the production kernels (cuobjdump -res-usage on
+    # the in-tree library): the envelope's register allocation is fragile (an
+    # extra kernel-parameter field once pushed its stack from 56 to 352 B and
+    # cost 23%), so the hot kernels' stack frames are pinned here
+    import shutil
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run(["cuobjdump", "-res-usage", sn.LIB_PATH], capture_output=True, text=True).stdout
+    usage, cur = {}, None
+    for line in out.splitlines():
+        m = re.match(r"\s*Function (\S+):", line)
+        if m:
+            cur = m.group(1)
+        m = re.search(r"REG:(\d+) STACK:(\d+)", line)
+        if m and cur:
+            usage[cur] = (int(m.group(1)), int(m.group(2)))
+    limits = {  # mangled name prefix -> max stack bytes
+        "_ZN3snb10k_envelopeIdLi2ELi4096ELb1E": 64,   # default FP64 envelope (N = 8192, FFT FIR)
+        "_ZN3snb10k_envelopeIfLi2ELi4096ELb1E": 0,
+        "_ZN3snb19k_envelope_pair2048IdE": 0,           # 1.5 m window
+        "_ZN3snb20k_envelope_split8192IdE": 32,         # 10 m window
+        "_ZN3snb13k_beamform_tcILi96E": 64,             # tensor-core delay-and-sum
+        "_ZN3snb7k_demod": 0,
+        "_ZN3snb10k_premf_rw": 0,
+    }
+    for prefix, lim in limits.items():
+        hits = [v for k, v in usage.items() if k.startswith(prefix)]
+        assert hits, prefix
+        assert all(st <= lim for _, st in hits), (prefix, hits)
