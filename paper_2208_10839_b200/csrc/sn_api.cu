@@ -139,6 +139,9 @@ struct sn_workspace {
     // (a device call on a caller stream followed by a host call, or two
     // device calls on different streams, share the scratch buffers)
     cudaEvent_t ev_last = nullptr;
+    // host path, blocks of one call: front end done (d_packed free), the
+    // block's downloads done (d_energy free)
+    cudaEvent_t ev_front = nullptr, ev_d2h = nullptr;
     void after_last(cudaStream_t s) const { ck(cudaStreamWaitEvent(s, ev_last, 0), "wait last"); }
     void mark_last(cudaStream_t s) const { ck(cudaEventRecord(ev_last, s), "record last"); }
     static constexpr int kMaxChunks = 16;
@@ -278,6 +281,8 @@ struct sn_workspace {
         if (s_env2) cudaStreamDestroy(s_env2);
         if (ev_beams) cudaEventDestroy(ev_beams);
         if (ev_last) cudaEventDestroy(ev_last);
+        if (ev_front) cudaEventDestroy(ev_front);
+        if (ev_d2h) cudaEventDestroy(ev_d2h);
         for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
                         (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot,  (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
@@ -315,6 +320,8 @@ struct sn_workspace {
         ck(cudaStreamCreateWithFlags(&s_env2, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaEventCreateWithFlags(&ev_beams, cudaEventDisableTiming), "cudaEventCreate");
         ck(cudaEventCreateWithFlags(&ev_last, cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&ev_front, cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&ev_d2h, cudaEventDisableTiming), "cudaEventCreate");
         for (int j = 0; j < kMaxChunks; ++j) {
             ck(cudaEventCreateWithFlags(&ev_in[j], cudaEventDisableTiming), "cudaEventCreate");
             ck(cudaEventCreateWithFlags(&ev_done[j], cudaEventDisableTiming), "cudaEventCreate");
@@ -949,12 +956,15 @@ struct sn_workspace {
     // sub-chunk's stream and returns its launch count. A later chunk's
     // delay-and-sum waits until the ring's previous contents are read.
     template <typename After>
-    uint64_t enqueue_per_direction(uint64_t c, After&& after) {
+    uint64_t enqueue_per_direction(uint64_t c, After&& after, cudaEvent_t energies_free = nullptr) {
         uint64_t nlaunch = 0, ev_j = 0;
         for (uint64_t o = 0; o < c; o += chunk_cap) {
             const uint64_t kc = std::min(chunk_cap, c - o);
             enqueue_beams(o, kc, stream);
             nlaunch += beam_launches();
+            // the energies buffer may still be read by the previous block's
+            // downloads: the envelope (not the delay-and-sum) waits for them
+            if (energies_free && o == 0) ck(cudaStreamWaitEvent(stream, energies_free, 0), "wait");
             ck(cudaEventRecord(ev_beams, stream), "event");
             ck(cudaStreamWaitEvent(s_env2, ev_beams, 0), "wait");
             const std::vector<uint64_t> chunks = env_chunks(kc);
@@ -986,9 +996,18 @@ struct sn_workspace {
         require_device();
         DeviceGuard g(device);
         const bool out_pinned = is_pinned(out);
+        bool in_pinned = true;
+        for (uint64_t i = 0; i < count && in_pinned; ++i) in_pinned = is_pinned(ms[i].packed);
+        // with page-locked caller buffers the blocks of a call pipeline into
+        // each other (block j + 1's upload and front end run under block j's
+        // envelope and downloads; ordered by events on the buffers they
+        // share); otherwise each block ends with a host synchronisation
+        // (the staging buffers are reused)
+        const bool pipelined = out_pinned && in_pinned;
         after_last(s_h2d);
         after_last(stream);
         uint64_t done = 0;
+        bool first = true;
         while (done < count) {
             const uint64_t c = std::min(max_batch, count - done);
             // captures uploaded in up to 4 parts (copy stream), the front end
@@ -998,12 +1017,13 @@ struct sn_workspace {
             // computes: only the first part's upload and the last chunk's
             // download are exposed
             const uint64_t parts = std::min<uint64_t>(c, 4);
+            if (!first) ck(cudaStreamWaitEvent(s_h2d, ev_front, 0), "wait"); // d_packed consumed
             uint64_t p0 = 0;
             for (uint64_t p = 0; p < parts; ++p) {
                 const uint64_t p1 = c * (p + 1) / parts;
                 for (uint64_t i = p0; i < p1; ++i) {
                     const uint8_t* src = ms[done + i].packed;
-                    if (!is_pinned(src)) {
+                    if (!in_pinned) {
                         std::memcpy(h_in + i * packed_bytes, src, packed_bytes);
                         src = h_in + i * packed_bytes;
                     }
@@ -1015,6 +1035,7 @@ struct sn_workspace {
                 enqueue_front(d_packed + p0 * packed_bytes, p0, p1 - p0, stream);
                 p0 = p1;
             }
+            ck(cudaEventRecord(ev_front, stream), "event");
             const uint64_t nlaunch = enqueue_per_direction(c, [&](uint64_t o, uint64_t k, cudaStream_t cs, cudaEvent_t ed) {
                 float* d_e = d_energy + o * energy_per;
                 ck(cudaEventRecord(ed, cs), "event");
@@ -1022,13 +1043,18 @@ struct sn_workspace {
                 float* dst = (out_pinned ? out + done * energy_per : h_out) + o * energy_per;
                 ck(cudaMemcpyAsync(dst, d_e, k * energy_per * sizeof(float), cudaMemcpyDeviceToHost, s_d2h), "D2H");
                 return uint64_t{0};
-            });
+            }, first ? nullptr : ev_d2h);
+            ck(cudaEventRecord(ev_d2h, s_d2h), "event");
             ck(cudaGetLastError(), "kernel launch");
             last_launches = 3 * parts + nlaunch;
-            ck(cudaStreamSynchronize(s_d2h), "process sync");
-            if (!out_pinned) std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
+            if (!pipelined) {
+                ck(cudaStreamSynchronize(s_d2h), "process sync");
+                if (!out_pinned) std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
+            }
             done += c;
+            first = false;
         }
+        if (pipelined) ck(cudaStreamSynchronize(s_d2h), "process sync");
         mark_last(s_d2h);
     }
 

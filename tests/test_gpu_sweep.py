@@ -259,3 +259,23 @@ def test_opt_in_log_normalisation_transform(gpu, po, ref):
                 assert got[i].max() == 1.0
     with pytest.raises(sn.ArgumentError):
         sn.energyscape_transform(e.data_ptr(), e.data_ptr(), 2, cells)
+
+
+def test_pipelined_host_blocks_match_single_calls(gpu):
+    # page-locked buffers: the blocks of one sn_workspace_process_batch call
+    # pipeline into each other (events on d_packed / d_energy); results equal
+    # one capture per call, and the pageable path (per-block sync) agrees
+    import torch
+    sn = gpu
+    cfg = cfg_for(sn, "box1850")
+    ms = [capture(sn, cfg, [(1.0 + 0.25 * i, 0.3 - 0.1 * i, 0.05, 0.7)], 0.01, 120 + i, seq=i) for i in range(7)]
+    ws = sn.Workspace(cfg, device=0, max_batch=2)  # 7 captures -> 4 blocks (2, 2, 2, 1)
+    pin_in = torch.from_numpy(np.stack([m.packed for m in ms])).pin_memory()
+    pin_out = torch.zeros((7, ws.n_dirs, ws.bins), dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        ws.process_packed_host(pin_in.numpy(), pin_out.numpy())
+        one = sn.Workspace(cfg, device=0, max_batch=1)
+        for i in (0, 3, 6):
+            assert np.array_equal(one.process(ms[i]).energies, pin_out.numpy()[i])
+    pageable = np.stack([im.energies for im in ws.process_batch(ms)])
+    assert np.array_equal(pageable, pin_out.numpy())
