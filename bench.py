@@ -81,6 +81,7 @@ def parse_args():
     p.add_argument("--sweep-steps", type=int, default=3)
     p.add_argument("--only-sweep", action="store_true", help="developer: print the sweep alone")
     p.add_argument("--lib", default=None, help="developer A/B: another build of libsonarnet_b200.so")
+    p.add_argument("--tc-tile-n", type=int, default=0, help="developer: tensor-core tile width (0: default)")
     return p.parse_args()
 
 
@@ -449,7 +450,7 @@ def run_b200(args):
     cfg = make_config(sn, args.grid, args.precision)
     B = args.batch
     pool_n = max(B, (args.pool // B) * B)
-    ws = sn.Workspace(cfg, device=local, max_batch=B)
+    ws = sn.Workspace(cfg, device=local, max_batch=B, tc_tile_n=args.tc_tile_n)
     d = ws.dims
     serial = rank + 1
     pool_h = synth_pool(sn, cfg, serial, pool_n)

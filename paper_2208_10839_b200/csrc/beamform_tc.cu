@@ -111,9 +111,9 @@ __device__ __forceinline__ uint32_t elect_one() {
     return pred;
 }
 
-// Y * 2^e (|Y| < 2^53, exact) assembled with integer instructions only: the
-// FP64 pipe is busy (math-throttled) while the tensor core runs, the integer
-// ALUs are not.
+// Y * 2^e (|Y| < 2^53, exact) assembled with integer instructions only (the
+// FP64 pipe shares its issue with the tensor pipe); the default epilogue uses
+// the hardware I2F.F64.S64 conversion instead (SNB_TC_INT_LDEXP: this one).
 __device__ __forceinline__ double i64_ldexp_exact(long long Y, int e) {
     const unsigned long long m = (unsigned long long)(Y < 0 ? -Y : Y);
     const int lz = __clzll(m | 1ull);
@@ -301,9 +301,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
                 (((size_t)b * a.clusters + c) * 12 * a.rows + (size_t)(a.pad + tt * TN - (R - 1))) * 16;
             uint8_t* dst = Bw + (size_t)(g % kWin) * bbuf;
             if (leader) {
+#ifdef SNB_TC_EXP_NOLOAD
+                // timing experiment only (wrong results): windows after the
+                // first kWin are not fetched
+                if (g >= kWin) {
+                    mbar_arrive(&wfull[g % kWin]);
+                } else
+#endif
+                {
                 mbar_expect_tx(&wfull[g % kWin], 12 * bytes);
                 for (int jh = 0; jh < 12; ++jh)
                     bulk_g2s(dst + (size_t)jh * wrows * 16, pb + (size_t)jh * a.rows * 16, bytes, &wfull[g % kWin]);
+                }
             }
             __syncwarp();
         };
@@ -407,6 +416,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
                 mbar_wait(&sfull[sl], (uint32_t)((q / kSlots) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                 const uint32_t src = tmem + lane_base + (uint32_t)(sl * TN + colq * NC);
+#ifdef SNB_TC_EXP_NOEPI
+                // timing experiment only (wrong results): handshakes alone
+                if (true) {
+                    (void)src;
+                    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sempty[sl]);
+                    continue;
+                }
+#endif
                 if constexpr (!kPark) {
                     uint32_t y[NC];
 #pragma unroll
@@ -444,6 +463,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
                 }
             }
             if (!live) continue;
+#ifdef SNB_TC_EXP_NOEPI
+            continue;
+#endif
 #pragma unroll
             for (int h = 0; h < NC / 16 + (NC % 16 ? 1 : 0); ++h) {
                 int32_t hi[16];
@@ -465,8 +487,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
                     if (16 * h + i0 >= NC) break;
                     double v[8];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                    for (int i = 0; i < 8; ++i) {
+#ifndef SNB_TC_INT_LDEXP
+                        // hardware int64 -> FP64 conversion (I2F.F64.S64, exact:
+                        // |Y| < 2^53; not on the FP64/tensor pipe), then the
+                        // power-of-two scale as an exponent add: 6 instructions
+                        // per output instead of ~17 for the integer-only
+                        // assembly (beamform stage 1.29 -> 1.16 ms, A/B)
+                        const long long Y = (long long)hi[i0 + i] * 16777216LL + yl[16 * h + i0 + i];
+                        const long long bits = __double_as_longlong(__ll2double_rn(Y)) + ((long long)eadj << 52);
+                        v[i] = Y ? __longlong_as_double(bits) : 0.0;
+#else
                         v[i] = i64_ldexp_exact((long long)hi[i0 + i] * 16777216LL + yl[16 * h + i0 + i], eadj);
+#endif
+                    }
                     const int64_t n0 = (int64_t)tt * TN + colq * NC + 16 * h + i0;
                     if (a.f32) {
                         float* out = reinterpret_cast<float*>(a.beams) + ((size_t)b * a.n_dirs + slot) * a.N + n0;

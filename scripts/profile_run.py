@@ -8,7 +8,10 @@ p = argparse.ArgumentParser()
 p.add_argument("--grid", default="hemisphere3000"); p.add_argument("--batch", type=int, default=1)
 p.add_argument("--iters", type=int, default=3); p.add_argument("--precision", default="f64")
 p.add_argument("--max-range", type=float, default=5.0)
+p.add_argument("--lib", default=None)
 a = p.parse_args()
+if a.lib:
+    sn.load_library(a.lib)
 kind = {"horizontal90": 0, "box1850": 1, "hemisphere3000": 2}[a.grid]
 cfg = sn.default_pipeline_config(kind).copy(precision=0 if a.precision == "f64" else 1, max_range=a.max_range)
 ws = sn.Workspace(cfg, device=0, max_batch=a.batch)
