@@ -494,7 +494,11 @@ __global__ void __launch_bounds__(kThreads * G, (M >= 8192 || M <= 2048) ? 1 : (
 #ifndef SNB_PRE
 #define SNB_PRE 2
 #endif
-    constexpr int kPre = SNB_PRE; // of the 16 inputs per thread; envelope ms by depth 0-4: 3.56, 3.48, 3.48, 3.60, 3.59 (8+: spills)
+    // of the 16 inputs per thread; direct-FIR path, envelope ms by depth 0-4:
+    // 3.56, 3.48, 3.48, 3.60, 3.59 (8+: spills); the FFT-FIR path loads them
+    // after its FIR, where depth 0 / 2 / 4 measured 2.95 / 3.04 / 3.05 ms
+    // (stack 8 / 56 / 88 B): none
+    constexpr int kPre = FF ? 0 : SNB_PRE;
     V pre[16];
     auto load_pre = [&](int64_t item) {
         const V* s = reinterpret_cast<const V*>(a.beams) + (size_t)item * M;
