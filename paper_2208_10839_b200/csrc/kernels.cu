@@ -514,7 +514,10 @@ __global__ void __launch_bounds__(kThreads * G, (M >= 8192 || M <= 2048) ? 1 : (
 #ifndef SNB_NO_BEAM_PREFETCH
         {
             // pull the next item's beam (N reals) into L2 while this one runs
-            const int64_t nx = it + (int64_t)gridDim.x * G;
+#ifndef SNB_PF_AHEAD
+#define SNB_PF_AHEAD 1
+#endif
+            const int64_t nx = it + (int64_t)gridDim.x * G * SNB_PF_AHEAD;
             if (nx < items && tid == 0) {
                 const R* nsrc = reinterpret_cast<const R*>(a.beams) + (size_t)nx * N;
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nsrc), "r"((unsigned)(N * sizeof(R)))
