@@ -52,7 +52,7 @@ TC_INT8_PEAK = 4500.0
 # the CPU reference runs with a test-only radix-2 FFTW-API stand-in
 # (oracle/fftw_shim), slower than FFTW on the FFT-bound stages, so GPU/CPU
 # ratios overstate the gap to a real-FFTW build by an unknown factor
-E2E_BLOCKS = 4  # device batches per host-API call in the e2e leg
+E2E_BLOCKS = 8  # device batches per host-API call in the e2e leg
 FFT_LABEL = "radix2-shim (oracle/fftw_shim; FFTW3 absent from the image)"
 
 

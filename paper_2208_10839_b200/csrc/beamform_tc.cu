@@ -73,6 +73,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// mbarrier wait that parks the warp (suspend-time hint) instead of re-polling:
+// the epilogue warps share the MMA warp's sub-partition, and their polling
+// loops take issue slots from it
+__device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
+#ifdef SNB_TC_PARK_NS
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "SNB_PARK_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra SNB_PARK_%=;\n}\n" ::"r"(su32(bar)),
+        "r"(parity), "r"((uint32_t)SNB_TC_PARK_NS)
+        : "memory");
+#else
+    mbar_wait(bar, parity);
+#endif
+}
+
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accumulate) {
     asm volatile(
@@ -365,7 +382,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
             for (int p = 0; p < kTcSlices; ++p) {
                 const int j = kTcSlices - 1 - p;
                 const int q = kTcSlices * g + p, sl = q % kSlots;
+#ifndef SNB_TC_EXP_NOSLOTWAIT
                 if (q >= kSlots) mbar_wait(&sempty[sl], (uint32_t)(((q - kSlots) / kSlots) & 1));
+#endif
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                 if (leader) {
                     uint64_t ad = a0;
@@ -413,7 +432,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
 #pragma unroll
             for (int p = 0; p < kTcSlices; ++p) {
                 const int q = kTcSlices * g + p, sl = q % kSlots;
-                mbar_wait(&sfull[sl], (uint32_t)((q / kSlots) & 1));
+                mbar_wait_park(&sfull[sl], (uint32_t)((q / kSlots) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                 const uint32_t src = tmem + lane_base + (uint32_t)(sl * TN + colq * NC);
 #ifdef SNB_TC_EXP_NOEPI
