@@ -956,7 +956,8 @@ struct sn_workspace {
     // sub-chunk's stream and returns its launch count. A later chunk's
     // delay-and-sum waits until the ring's previous contents are read.
     template <typename After>
-    uint64_t enqueue_per_direction(uint64_t c, After&& after, cudaEvent_t energies_free = nullptr) {
+    uint64_t enqueue_per_direction(uint64_t c, After&& after, cudaEvent_t energies_free = nullptr,
+                                   bool one_envelope = false) {
         uint64_t nlaunch = 0, ev_j = 0;
         for (uint64_t o = 0; o < c; o += chunk_cap) {
             const uint64_t kc = std::min(chunk_cap, c - o);
@@ -967,7 +968,9 @@ struct sn_workspace {
             if (energies_free && o == 0) ck(cudaStreamWaitEvent(stream, energies_free, 0), "wait");
             ck(cudaEventRecord(ev_beams, stream), "event");
             ck(cudaStreamWaitEvent(s_env2, ev_beams, 0), "wait");
-            const std::vector<uint64_t> chunks = env_chunks(kc);
+            // one envelope launch when a later block of the same call hides
+            // this block's downloads; else sub-chunks that overlap them
+            const std::vector<uint64_t> chunks = one_envelope ? std::vector<uint64_t>{kc} : env_chunks(kc);
             uint64_t off = 0;
             for (uint64_t j = 0; j < chunks.size(); ++j, ++ev_j) {
                 const uint64_t k = chunks[j];
@@ -1043,7 +1046,7 @@ struct sn_workspace {
                 float* dst = (out_pinned ? out + done * energy_per : h_out) + o * energy_per;
                 ck(cudaMemcpyAsync(dst, d_e, k * energy_per * sizeof(float), cudaMemcpyDeviceToHost, s_d2h), "D2H");
                 return uint64_t{0};
-            }, first ? nullptr : ev_d2h);
+            }, first ? nullptr : ev_d2h, pipelined && done + c < count);
             ck(cudaEventRecord(ev_d2h, s_d2h), "event");
             ck(cudaGetLastError(), "kernel launch");
             last_launches = 3 * parts + nlaunch;
