@@ -141,7 +141,8 @@ struct sn_workspace {
     cudaEvent_t ev_last = nullptr;
     // host path, blocks of one call: front end done (d_packed free), the
     // block's downloads done (d_energy free)
-    cudaEvent_t ev_front = nullptr, ev_d2h = nullptr;
+    cudaEvent_t ev_front = nullptr, ev_d2h[2] = {};
+    float* d_energy_cur = nullptr; // the half the current block's envelope writes
     void after_last(cudaStream_t s) const { ck(cudaStreamWaitEvent(s, ev_last, 0), "wait last"); }
     void mark_last(cudaStream_t s) const { ck(cudaEventRecord(ev_last, s), "record last"); }
     static constexpr int kMaxChunks = 16;
@@ -282,7 +283,8 @@ struct sn_workspace {
         if (ev_beams) cudaEventDestroy(ev_beams);
         if (ev_last) cudaEventDestroy(ev_last);
         if (ev_front) cudaEventDestroy(ev_front);
-        if (ev_d2h) cudaEventDestroy(ev_d2h);
+        for (cudaEvent_t e : ev_d2h)
+            if (e) cudaEventDestroy(e);
         for (void* p : {(void*)d_packed, (void*)d_demod, (void*)d_mf, (void*)d_filt,
                         (void*)d_filt32, (void*)d_beams, (void*)d_order, (void*)d_shifts_slot,  (void*)d_energy, (void*)d_lut, (void*)d_premf,
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
@@ -321,7 +323,7 @@ struct sn_workspace {
         ck(cudaEventCreateWithFlags(&ev_beams, cudaEventDisableTiming), "cudaEventCreate");
         ck(cudaEventCreateWithFlags(&ev_last, cudaEventDisableTiming), "cudaEventCreate");
         ck(cudaEventCreateWithFlags(&ev_front, cudaEventDisableTiming), "cudaEventCreate");
-        ck(cudaEventCreateWithFlags(&ev_d2h, cudaEventDisableTiming), "cudaEventCreate");
+        for (cudaEvent_t& e : ev_d2h) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
         for (int j = 0; j < kMaxChunks; ++j) {
             ck(cudaEventCreateWithFlags(&ev_in[j], cudaEventDisableTiming), "cudaEventCreate");
             ck(cudaEventCreateWithFlags(&ev_done[j], cudaEventDisableTiming), "cudaEventCreate");
@@ -357,7 +359,9 @@ struct sn_workspace {
         upload(d_order, plan.order, stream);
         upload(d_shifts_slot, plan.shifts, stream);
 
-        d_energy = dmalloc<float>(B * energy_per, n);
+        // two halves: consecutive blocks of one host-path call alternate, so
+        // block j's downloads overlap block j + 1's kernels
+        d_energy = dmalloc<float>(2 * B * energy_per, n);
         d_lut = dmalloc<double>(plan.demod_lut.size(), n);
         d_premf = dmalloc<double>(plan.premf_rev.size(), n);
         d_comp = dmalloc<double>(plan.comp_rev.size(), n);
@@ -956,8 +960,7 @@ struct sn_workspace {
     // sub-chunk's stream and returns its launch count. A later chunk's
     // delay-and-sum waits until the ring's previous contents are read.
     template <typename After>
-    uint64_t enqueue_per_direction(uint64_t c, After&& after, cudaEvent_t energies_free = nullptr,
-                                   bool one_envelope = false) {
+    uint64_t enqueue_per_direction(uint64_t c, After&& after, cudaEvent_t energies_free = nullptr) {
         uint64_t nlaunch = 0, ev_j = 0;
         for (uint64_t o = 0; o < c; o += chunk_cap) {
             const uint64_t kc = std::min(chunk_cap, c - o);
@@ -968,14 +971,15 @@ struct sn_workspace {
             if (energies_free && o == 0) ck(cudaStreamWaitEvent(stream, energies_free, 0), "wait");
             ck(cudaEventRecord(ev_beams, stream), "event");
             ck(cudaStreamWaitEvent(s_env2, ev_beams, 0), "wait");
-            // one envelope launch when a later block of the same call hides
-            // this block's downloads; else sub-chunks that overlap them
-            const std::vector<uint64_t> chunks = one_envelope ? std::vector<uint64_t>{kc} : env_chunks(kc);
+            // sub-chunks on two streams (measured: also for the inner blocks of
+            // a pipelined call, where one launch per block was 2% slower: the
+            // next block's front end starts under the other stream's tail)
+            const std::vector<uint64_t> chunks = env_chunks(kc);
             uint64_t off = 0;
             for (uint64_t j = 0; j < chunks.size(); ++j, ++ev_j) {
                 const uint64_t k = chunks[j];
                 cudaStream_t cs = (j & 1) ? s_env2 : stream;
-                enqueue_envelope(off, k, d_energy + (o + off) * energy_per, cs);
+                enqueue_envelope(off, k, (d_energy_cur ? d_energy_cur : d_energy) + (o + off) * energy_per, cs);
                 nlaunch += 1 + after(o + off, k, cs, ev_done[ev_j % kMaxChunks]);
                 off += k;
             }
@@ -1009,10 +1013,11 @@ struct sn_workspace {
         const bool pipelined = out_pinned && in_pinned;
         after_last(s_h2d);
         after_last(stream);
-        uint64_t done = 0;
-        bool first = true;
+        uint64_t done = 0, blk = 0;
         while (done < count) {
             const uint64_t c = std::min(max_batch, count - done);
+            const int half = (int)(blk & 1);
+            float* d_en = d_energy + (uint64_t)half * max_batch * energy_per;
             // captures uploaded in up to 4 parts (copy stream), the front end
             // of part p running while part p + 1 is on the bus; the
             // beamformer for the whole block; then the envelope in chunks whose
@@ -1020,7 +1025,7 @@ struct sn_workspace {
             // computes: only the first part's upload and the last chunk's
             // download are exposed
             const uint64_t parts = std::min<uint64_t>(c, 4);
-            if (!first) ck(cudaStreamWaitEvent(s_h2d, ev_front, 0), "wait"); // d_packed consumed
+            if (blk > 0) ck(cudaStreamWaitEvent(s_h2d, ev_front, 0), "wait"); // d_packed consumed
             uint64_t p0 = 0;
             for (uint64_t p = 0; p < parts; ++p) {
                 const uint64_t p1 = c * (p + 1) / parts;
@@ -1039,15 +1044,17 @@ struct sn_workspace {
                 p0 = p1;
             }
             ck(cudaEventRecord(ev_front, stream), "event");
+            d_energy_cur = d_en;
             const uint64_t nlaunch = enqueue_per_direction(c, [&](uint64_t o, uint64_t k, cudaStream_t cs, cudaEvent_t ed) {
-                float* d_e = d_energy + o * energy_per;
+                float* d_e = d_en + o * energy_per;
                 ck(cudaEventRecord(ed, cs), "event");
                 ck(cudaStreamWaitEvent(s_d2h, ed, 0), "wait");
                 float* dst = (out_pinned ? out + done * energy_per : h_out) + o * energy_per;
                 ck(cudaMemcpyAsync(dst, d_e, k * energy_per * sizeof(float), cudaMemcpyDeviceToHost, s_d2h), "D2H");
                 return uint64_t{0};
-            }, first ? nullptr : ev_d2h, pipelined && done + c < count);
-            ck(cudaEventRecord(ev_d2h, s_d2h), "event");
+            }, blk >= 2 ? ev_d2h[half] : nullptr);
+            d_energy_cur = nullptr;
+            ck(cudaEventRecord(ev_d2h[half], s_d2h), "event"); // this half's downloads
             ck(cudaGetLastError(), "kernel launch");
             last_launches = 3 * parts + nlaunch;
             if (!pipelined) {
@@ -1055,7 +1062,7 @@ struct sn_workspace {
                 if (!out_pinned) std::memcpy(out + done * energy_per, h_out, c * energy_per * sizeof(float));
             }
             done += c;
-            first = false;
+            ++blk;
         }
         if (pipelined) ck(cudaStreamSynchronize(s_d2h), "process sync");
         mark_last(s_d2h);
