@@ -69,7 +69,7 @@ def parse_args():
     p.add_argument("--gather", action="store_true", help="NCCL 360-degree gather per step")
     p.add_argument("--latency-samples", type=int, default=50)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-calls", type=int, default=2, help="reference calls per host thread")
+    p.add_argument("--cpu-calls", type=int, default=8, help="reference calls per host thread (~5-10 s of CPU work)")
     p.add_argument("--stream-frames", type=int, default=2048,
                    help="frames of the 8-sensor streaming run through the worker pool (configs[3]: 256 "
                         "measurements x 8 sensors; 0: skip)")
