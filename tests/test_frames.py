@@ -103,6 +103,19 @@ def test_process_frames_errors_like_the_central_node(sn, po, ref):
         assert f[36:-4].decode() == e.value.msg                           # the reference's message
     with pytest.raises(po.OracleError):
         rws.process_frame(bytes(bad_crc))
+    # a nominal-size frame whose header is corrupted (pdm_rate byte flipped,
+    # CRC no longer matching): the reference checks the CRC first and drops
+    # it as an integrity error (wire.cpp:136-145) -- discarded, not an error
+    # frame carrying the corrupted ids
+    bad_rate_crc = bytearray(good)
+    bad_rate_crc[66 + 6] ^= 0x01          # a byte of the f64 pdm_rate field
+    bad_serial = bytearray(good)
+    bad_serial[36] ^= 0x55                # the payload's sensor serial
+    got = ws.process_frames([bytes(bad_rate_crc), bytes(bad_serial), good])
+    assert [s for s, _ in got] == [4, 4, 0] and got[0][1] == b"" and got[1][1] == b""
+    for f in (bad_rate_crc, bad_serial):
+        with pytest.raises(po.OracleError):
+            rws.process_frame(bytes(f))
 
 
 # ---------------------------------------------------------------------------
