@@ -32,7 +32,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr
                      "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v"]
 
 CU_SOURCES = ["kernels.cu", "beamform_tc.cu", "frames.cu", "synth.cu", "sn_api.cu"]
-CPP_SOURCES = ["plan.cpp", "pool.cpp", "gather.cpp"]
+CPP_SOURCES = ["plan.cpp", "cluster.cpp", "pool.cpp", "gather.cpp"]
 HEADERS = ["fft.cuh", "kernels.cuh", "plan.hpp"]
 
 

@@ -448,6 +448,9 @@ Plan make_plan(const sn_pipeline_config& cin) {
         };
         split(split, idx.data(), idx.data() + idx.size(), false);
         tc_leaves.push_back((int32_t)s.n_dirs);
+        // tensor-core clusters: balanced k-means in the shift vectors' 2-D
+        // embedding when that lowers the MMA work (cluster.cpp)
+        rebalance_tc_clusters(p, s.n_dirs, leaves, tc_leaves);
         p.tc_leaves = std::move(tc_leaves);
         std::vector<std::pair<uint64_t, int32_t>> keyed(s.n_dirs);
         for (uint64_t k = 0; k < s.n_dirs; ++k) keyed[k] = {k, leaves[k]};

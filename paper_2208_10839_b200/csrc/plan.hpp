@@ -65,6 +65,9 @@ constexpr int kTcLeafDirs = 128; // upper k-d level: tensor-core beamformer clus
 // Validates (pipeline.cpp:60-92; geometry.cpp:27-57 invariants; Direction
 // ranges geometry.cpp:146-155) and derives every table. Throws Error.
 Plan make_plan(const sn_pipeline_config& cfg);
+// tensor-core cluster planning (cluster.cpp): replaces the k-d leaves and the
+// cluster bounds by balanced k-means clusters when that lowers the sum of R_c
+void rebalance_tc_clusters(Plan& p, uint64_t n, std::vector<int32_t>& leaves, std::vector<int32_t>& tc_leaves);
 Sizes derive_sizes(const sn_pipeline_config& cfg); // validate + sizes only
 
 // Setup helpers restated from the reference.

@@ -8,7 +8,7 @@ C=$ROOT/paper_2208_10839_b200/csrc
 O=$ROOT/paper_2208_10839_b200/_lib/ab/$1
 mkdir -p $O
 ARCH="-gencode arch=compute_100a,code=sm_100a"
-for f in plan pool gather; do g++ -O2 -std=c++17 -fPIC -ffp-contract=off -I $ROOT/include -I $C -I /usr/local/cuda/include -c $C/$f.cpp -o $O/$f.o; done
+for f in plan cluster pool gather; do g++ -O2 -std=c++17 -fPIC -ffp-contract=off -I $ROOT/include -I $C -I /usr/local/cuda/include -c $C/$f.cpp -o $O/$f.o; done
 pids=()
 for f in kernels beamform_tc frames synth sn_api; do
   nvcc $ARCH -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-ffp-contract=off $2 -I $ROOT/include -I $C -c $C/$f.cu -o $O/$f.o &
