@@ -352,7 +352,9 @@ void sn_gather_destroy(sn_gather* g);
  * gather `count` images (count x image_floats f32, device) and their ids
  * (host) from every rank into slot `slot` (0/1) of rank 0's d_view (device,
  * world x count x image_floats, rank-major; ignored elsewhere). Returns once
- * enqueued; collective: every rank calls it with the same slot and count. */
+ * enqueued (after waiting on the host for the slot's previous gather, whose
+ * id staging it reuses); collective: every rank calls it with the same slot
+ * and count. */
 sn_status sn_gather_start(sn_gather* g, int slot, const float* d_images, const sn_frame_id* ids, uint64_t count,
                           float* d_view, void* stream);
 /* Make `stream` wait for slot's last gather (NULL: block the host) — call

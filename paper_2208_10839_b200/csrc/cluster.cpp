@@ -47,7 +47,9 @@ int64_t cluster_R_sum(const std::vector<int32_t>& sh /* dir-major n x 32 */, con
 } // namespace
 
 void rebalance_tc_clusters(Plan& p, uint64_t n, std::vector<int32_t>& leaves, std::vector<int32_t>& tc_leaves) {
-    if (n <= (uint64_t)kTcLeafDirs) return;
+    // (beyond ~40k directions the O(n K) Lloyd iterations would dominate
+    // workspace creation: keep the k-d clusters there)
+    if (n <= (uint64_t)kTcLeafDirs || n > 40000) return;
     std::vector<int32_t> sh(n * kCh);
     for (uint64_t d = 0; d < n; ++d)
         for (int i = 0; i < kCh; ++i) sh[d * kCh + i] = p.delays[d * kCh + i] - p.advances[d];
