@@ -10,7 +10,7 @@
 // sheet, where a k-d split makes boxes whose diagonal sets R. Balanced k-means
 // (capacity kTcLeafDirs) on the top-2 principal components, three
 // deterministic restarts, keeping whichever clustering -- k-d or k-means --
-// has the smaller sum of R_c (hemisphere3000: 405 -> ~350). Members keep their
+// has the smaller sum of R_c (hemisphere3000: 405 -> 362). Members keep their
 // k-d order (locality for the 8-direction leaves of the CUDA-core path).
 #include "plan.hpp"
 
