@@ -444,7 +444,7 @@ __device__ __forceinline__ void fir_polyphase(const R* ph, const R* comp, const 
 template <typename R, int G, int M, bool FF = false>
 // (M <= 2048 generic fallbacks -- the 1.5 m window runs k_envelope_pair2048 --
 // get the full register file: at 128 registers their Stockham passes spilled)
-__global__ void __launch_bounds__(kThreads * G, (M >= 8192 || M <= 2048) ? 1 : (sizeof(R) == 8 ? SNB_ENV_MINB : SNB_ENV_MINB_F32) / G)
+__global__ void __launch_bounds__(kThreads * G, (M >= 8192 || M <= 2048) ? 1 : ((sizeof(R) == 8 ? SNB_ENV_MINB : SNB_ENV_MINB_F32) / G > 0 ? (sizeof(R) == 8 ? SNB_ENV_MINB : SNB_ENV_MINB_F32) / G : 1))
     k_envelope(EnvArgs a, FirTaps<R> taps) {
     static_assert(!FF || M == 4096, "FFT FIR: N = 8192 only");
     using V = typename Cx<R>::T;
@@ -1284,15 +1284,17 @@ static void env_launch(const EnvArgs& a, const FirTaps<R>& taps, int grid, size_
 // factors and twiddles in shared memory
 size_t envelope_ff_smem_bytes(bool f32) {
     const size_t rb = f32 ? 4 : 8;
-    return ((size_t)kTwSharedCount + kFfU + kFfW) * 2 * rb + (size_t)kFfGroups * envelope_group_reals(8192, 0) * rb;
+    return ((size_t)kTwSharedCount + kFfU + kFfW) * 2 * rb +
+           (size_t)(f32 ? kFfGroupsF32 : kFfGroups) * envelope_group_reals(8192, 0) * rb;
 }
 
 int envelope_ff_blocks_per_sm(bool f32) {
     int n = 1;
     const size_t smem = envelope_ff_smem_bytes(f32);
     if (f32) {
-        set_smem((const void*)k_envelope<float, kFfGroups, 4096, true>, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_envelope<float, kFfGroups, 4096, true>, kThreads * kFfGroups, smem);
+        set_smem((const void*)k_envelope<float, kFfGroupsF32, 4096, true>, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_envelope<float, kFfGroupsF32, 4096, true>, kThreads * kFfGroupsF32,
+                                                      smem);
     } else {
         set_smem((const void*)k_envelope<double, kFfGroups, 4096, true>, smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_envelope<double, kFfGroups, 4096, true>, kThreads * kFfGroups, smem);
@@ -1303,8 +1305,9 @@ int envelope_ff_blocks_per_sm(bool f32) {
 template <typename R>
 static void env_ff_launch(const EnvArgs& a, const FirTaps<R>& taps, int grid, cudaStream_t s) {
     const size_t smem = envelope_ff_smem_bytes(sizeof(R) == 4);
-    set_smem((const void*)k_envelope<R, kFfGroups, 4096, true>, smem);
-    k_envelope<R, kFfGroups, 4096, true><<<grid, kThreads * kFfGroups, smem, s>>>(a, taps);
+    constexpr int G = ff_groups<R>();
+    set_smem((const void*)k_envelope<R, G, 4096, true>, smem);
+    k_envelope<R, G, 4096, true><<<grid, kThreads * G, smem, s>>>(a, taps);
 }
 
 int envelope_pair2048_blocks_per_sm(bool f32) {

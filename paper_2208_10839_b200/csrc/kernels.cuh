@@ -107,6 +107,11 @@ void launch_envelope(const EnvArgs& a, const FirTaps<float>& t32, const FirTaps<
                      int grid, cudaStream_t s);
 size_t envelope_smem_bytes(int n, int comp_taps_padded, int phase_reals, bool f32, int groups);
 constexpr int kFfGroups = 2;        // FFT FIR envelope: groups per CTA (shared factor tables)
+#ifndef SNB_FF_G32
+#define SNB_FF_G32 3 // FP32 envelope ms by groups per CTA: 2: 2.14, 3: 1.86, 4: 1.89 (64 registers: spills)
+#endif
+constexpr int kFfGroupsF32 = SNB_FF_G32; // FP32 mode: half the registers per value, more groups fit
+template <typename R> constexpr int ff_groups() { return sizeof(R) == 4 ? kFfGroupsF32 : kFfGroups; }
 size_t envelope_ff_smem_bytes(bool f32);
 int envelope_ff_blocks_per_sm(bool f32); // 0: does not fit
 __host__ __device__ int envelope_group_reals(int n, int phase_reals);
