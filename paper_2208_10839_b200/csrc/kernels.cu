@@ -332,18 +332,30 @@ __host__ __device__ int envelope_group_reals(int n, int phase_reals) {
     return (r + 1) & ~1;
 }
 
-// |b + iH(b)|. FP64: rsqrt seed from the SFU (~22 bits), one Newton step on
-// the reciprocal root (~44 bits) and one on the root itself (<= 1 ulp),
+// |b + iH(b)|. FP64: rsqrt seed from the SFU and one third-order step
 // instead of the correctly rounded library sequence; FP32: sqrtf.
 __device__ __forceinline__ double fast_sqrt(double x) {
-    // branch-free: FP64 approximate reciprocal root (MUFU.RSQ64H), one Newton
-    // step on the reciprocal, one on the root; x == 0 gives 0 (the seed input
-    // is clamped away from 0 so r stays finite)
+#ifdef SNB_SQRT_TWO_STEP
+    // (round-2 form: one Newton step on the reciprocal root, one on the root)
     double r;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(fmax(x, 1e-300)));
     r = r * fma(-0.5 * x, r * r, 1.5);
     const double s = x * r;
     return fma(0.5 * r, fma(-s, s, x), s);
+#else
+    // branch-free: seed r0 = rsqrt(x)(1 + d) from the SFU (MUFU.RSQ64H), s =
+    // x r0, e = s r0 - 1 = (1 + d)^2 - 1 (exact by FMA, so it also corrects
+    // the rounding of s), then s (1 + e)^(-1/2) to third order:
+    // s (1 - e/2 + 3 e^2 / 8), error ~2.5 d^3 -- six FP64 operations instead
+    // of eight plus a clamp (scripts/micro/rsqrt_acc.cu measures d and the
+    // result's error). x == 0 gives 0 (the seed input x + 1e-300 stays
+    // normal; it equals x for every x >= 2^-942).
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x + 1e-300));
+    const double s = x * r;
+    const double e = fma(s, r, -1.0);
+    return fma(s, e * fma(e, 0.375, -0.5), s);
+#endif
 }
 __device__ __forceinline__ float fast_sqrt(float x) { return sqrtf(x); }
 
