@@ -564,6 +564,23 @@ __device__ __forceinline__ void dit_pass3_4096(V* buf, const TW& tw, Sink sink) 
     for (int r = 0; r < 16; ++r) sink(m + 256 * out_slot<16>(r), v[r]);
 }
 
+// inverse stage C as above, the thread's whole output row handed to
+// sink(m, v) after the barrier: v[r] = z[m + 256 out_slot(r)]
+template <typename V, typename TW, typename Sink>
+__device__ __forceinline__ void dit_pass3_4096_row(V* buf, const TW& tw, Sink sink) {
+    const int m = gtid();
+    V v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = buf[pad16(256 * r + m)];
+    V w[16];
+    tw_powers(tw, 256, m, w);
+#pragma unroll
+    for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], cconj(w[r]));
+    dft16<true>(v);
+    gsync();
+    sink(m, v);
+}
+
 // ---------------------------------------------------------------------------
 // Smoothing FIR by FFT (the composite 447-tap filter at stride 10 of
 // pipeline.cpp:466-468, default shapes). In polyphase form the decimated
@@ -622,7 +639,10 @@ __device__ __forceinline__ void dft3(V& x0, V& x1, V& x2) {
 // out[o] = max(0, float(r[o])) for o < bins. U: [16][kFfThreads] in the
 // register order of the third forward pass; W: [w768^j, j < 256][w256^{n3 k2}
 // at 16 k2 + n3] (e^{-2 pi i . / n}); both in shared memory.
-template <typename V>
+// PASS1 == false: the first forward pass was done by the producer of the
+// layout (the envelope's fused sink, which holds the three samples of each
+// radix-3 butterfly in one thread).
+template <bool PASS1 = true, typename V>
 __device__ __forceinline__ void fir_fft768(V* buf, const V* U, const V* W, float* __restrict__ eo, int bins) {
     using R = decltype(V{}.x);
     int t = gtid();
@@ -631,7 +651,7 @@ __device__ __forceinline__ void fir_fft768(V* buf, const V* U, const V* W, float
     // spilling them
     asm volatile("" : "+r"(t));
     const V* w256 = W + 256;
-    {
+    if constexpr (PASS1) {
         // forward pass 1: radix 3 over n1, * w768^{j k1}, the five sequences
         const int j = t;
         const V w1 = W[j], w2 = cmul(w1, w1);
@@ -643,8 +663,8 @@ __device__ __forceinline__ void fir_fft768(V* buf, const V* U, const V* W, float
             buf[ff_slot(a, j + 256)] = cmul(x1, w1);
             buf[ff_slot(a, j + 512)] = cmul(x2, w2);
         }
+        gsync();
     }
-    gsync();
     if (t < kFfThreads) {
         // forward pass 2 (thread (a, k1, n3)): DFT16 over n2, * w256^{n3 k2}
         const int a = t / 48, rem = t - 48 * a, k1 = rem >> 4, n3 = rem & 15;

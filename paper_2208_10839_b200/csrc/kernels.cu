@@ -464,6 +464,11 @@ __global__ void __launch_bounds__(kThreads * G, (M >= 8192 || M <= 2048) ? 1 : (
     constexpr int N = 2 * M;
     const int grp = gidx(), tid = gtid();
     constexpr bool kSmemTw = M == kTwSharedM;
+#ifdef SNB_FF_NOFUSE
+    constexpr bool kFfFused = false;
+#else
+    constexpr bool kFfFused = FF; // the FIR's first pass in the sink
+#endif
     V* tws = reinterpret_cast<V*>(smem);                   // compact twiddles (M == 4096)
     // FF: the FFT FIR's spectrum factors and twiddles, shared by the groups
     V* ffu = tws + (kSmemTw ? kTwSharedCount : 0);
@@ -576,15 +581,74 @@ __global__ void __launch_bounds__(kThreads * G, (M >= 8192 || M <= 2048) ? 1 : (
                     if (2 * n + 1 < Li) ph[pp + 1 == D ? u + 1 : (pp + 1) * PL + u] = m1;
                 }
             };
+            // FFT FIR, fused: the sink also runs the FIR's first forward pass
+            // (radix 3 over u, u + 256, u + 512 of one sequence: samples
+            // t, t + 2560, t + 5120 = outputs k, k + 5, k + 10 of this
+            // thread's row, t_k = 2 m + c0 + 512 k) and writes every slot of
+            // the layout, zeros included. The thread's five butterflies start
+            // at the t_k in [0, 2560): k = 0..4 when t_0 < 512, else
+            // k = -1..3 (t_-1 < c0: that sample is a zero). k = 15 (t >= 7680)
+            // is never needed: by the host check (hi_a < 768) every sample
+            // with t >= 7680 lies past L. Needs c0 < 512 (implied by
+            // lo_a <= 32).
+            auto sink_row = [&](int m, V(&v)[16]) {
+                // opaque per item: the slots and twiddles below are
+                // loop-invariant, and hoisting them out of the item loop spills
+                asm volatile("" : "+r"(m));
+                const unsigned t0 = 2u * (unsigned)m + (unsigned)c0;
+                const bool hi = t0 >= 512u;
+                // (unconditional loads -- n < M, inside the item's beam -- so
+                // the compiler can issue them ahead; out-of-range samples
+                // selected to zero)
+                auto mag = [&](int k) -> V {
+                    const int n = m + 256 * k;
+                    const V h = v[out_slot<16>(k)];
+                    const V bv = __ldg(bsrc + n);
+                    const R m0 = fast_sqrt(bv.x * bv.x + h.x * h.x);
+                    const R m1 = fast_sqrt(bv.y * bv.y + h.y * h.y);
+                    return V{2 * n < Li ? m0 : (R)0, 2 * n + 1 < Li ? m1 : (R)0};
+                };
+#pragma unroll
+                for (int j = 0; j < 5; ++j) {
+                    V x0, x1, x2;
+                    unsigned t;
+                    if (j < 4) {
+                        x0 = mag(j);
+                        x1 = mag(j + 5);
+                        x2 = mag(j + 10);
+                        t = t0 + 512u * j;
+                    } else {
+                        const V a4 = mag(4), a9 = mag(9), a14 = mag(14);
+                        x0 = hi ? V{(R)0, (R)0} : a4;
+                        x1 = hi ? a4 : a9;
+                        x2 = hi ? a9 : a14;
+                        t = hi ? t0 - 512u : t0 + 2048u;
+                    }
+                    const unsigned u = __umulhi(t, dmagic); // t / 10 (< 256)
+                    const int sa = ((int)(t - 10u * u) - 1) >> 1;
+                    dft3<false>(x0, x1, x2);
+                    const V w1 = ffw[u], w2 = cmul(w1, w1);
+                    V* sl = bufB + ff_slot(sa, (int)u);
+                    sl[0] = x0;
+                    sl[272] = cmul(x1, w1); // pad16(u + 256) = pad16(u) + 272
+                    sl[544] = cmul(x2, w2);
+                    // (A/B: one butterfly at a time)
+#ifdef SNB_FF_FENCE
+                    asm volatile("" ::: "memory");
+#endif
+                }
+            };
             if constexpr (M == 4096) {
                 dit_pass2_4096(bufB, twsrc);
-                dit_pass3_4096(bufB, twsrc, sink);
+                if constexpr (kFfFused) dit_pass3_4096_row(bufB, twsrc, sink_row);
+                else dit_pass3_4096(bufB, twsrc, sink);
             } else {
                 cfft<M, true, true>(bufB, bufB, twsrc, sink);
             }
             // zero the slots whose sample lies outside [0, L): per phase row p,
             // u < ceil((c0 - p) / D) and u >= ceil((L + c0 - p) / D)
-            if constexpr (ffir) {
+            if constexpr (kFfFused) {
+            } else if constexpr (ffir) {
                 // slot (a, u) holds samples n = 10 u + 2 a + 1 - c0 and n + 1:
                 // zero for u < lo_a and u >= hi_a (at most 32 on either side,
                 // checked on the host)
@@ -615,7 +679,7 @@ __global__ void __launch_bounds__(kThreads * G, (M >= 8192 || M <= 2048) ? 1 : (
             if constexpr (FF) {
                 // (the next item's early first-pass loads come after the FFT FIR:
                 // its radix-16 passes need the whole register budget)
-                fir_fft768(bufB, ffu, ffw, eo, (int)a.bins);
+                fir_fft768<!kFfFused>(bufB, ffu, ffw, eo, (int)a.bins);
                 if (nx < items) load_pre(nx);
             } else {
                 fir_polyphase<R>(ph, comp, a, eo);
