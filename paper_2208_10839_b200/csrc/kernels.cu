@@ -334,30 +334,33 @@ __host__ __device__ int envelope_group_reals(int n, int phase_reals) {
 
 // |b + iH(b)|. FP64: rsqrt seed from the SFU and one third-order step
 // instead of the correctly rounded library sequence; FP32: sqrtf.
-__device__ __forceinline__ double fast_sqrt(double x) {
+__device__ __forceinline__ double fast_mag(double b, double h) {
 #ifdef SNB_SQRT_TWO_STEP
     // (round-2 form: one Newton step on the reciprocal root, one on the root)
+    const double x = b * b + h * h;
     double r;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(fmax(x, 1e-300)));
     r = r * fma(-0.5 * x, r * r, 1.5);
     const double s = x * r;
     return fma(0.5 * r, fma(-s, s, x), s);
 #else
-    // branch-free: seed r0 = rsqrt(x)(1 + d) from the SFU (MUFU.RSQ64H), s =
-    // x r0, e = s r0 - 1 = (1 + d)^2 - 1 (exact by FMA, so it also corrects
-    // the rounding of s), then s (1 + e)^(-1/2) to third order:
-    // s (1 - e/2 + 3 e^2 / 8), error ~2.5 d^3 -- six FP64 operations instead
-    // of eight plus a clamp (scripts/micro/rsqrt_acc.cu measures d and the
-    // result's error). x == 0 gives 0 (the seed input x + 1e-300 stays
-    // normal; it equals x for every x >= 2^-942).
+    // x = b^2 + h^2 + 2^-996: the tiny term keeps the seed finite at b = h = 0
+    // (result 2^-498, which every f32 output rounds away) and changes x for
+    // no x >= 2^-940. Seed r0 = rsqrt(x)(1 + d) from the SFU (MUFU.RSQ64H),
+    // s = x r0, e = s r0 - 1 = (1 + d)^2 - 1 (exact by FMA, so it also
+    // corrects the rounding of s), then s (1 + e)^(-1/2) to third order:
+    // s (1 - e/2 + 3 e^2 / 8), error ~2.5 d^3. Seven FP64 operations (the
+    // round-2 form: ten and a clamp); scripts/micro/rsqrt_acc.cu measures d
+    // and the result's error (max 2^-52 relative).
+    const double x = fma(b, b, fma(h, h, 0x1p-996));
     double r;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x + 1e-300));
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     const double s = x * r;
     const double e = fma(s, r, -1.0);
     return fma(s, e * fma(e, 0.375, -0.5), s);
 #endif
 }
-__device__ __forceinline__ float fast_sqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ float fast_mag(float b, float h) { return sqrtf(b * b + h * h); }
 
 // Composite smoothing/anti-alias FIR evaluated at stride D (the work of
 // detail::strided_filter, filters.hpp:14-39, at pipeline.cpp:466-468), in
@@ -567,8 +570,8 @@ __global__ void __launch_bounds__(kThreads * G, (M >= 8192 || M <= 2048) ? 1 : (
             constexpr bool ffir = FF;
             auto sink = [&](int n, V h) {
                 const V bv = __ldg(bsrc + n);
-                const R m0 = fast_sqrt(bv.x * bv.x + h.x * h.x);
-                const R m1 = fast_sqrt(bv.y * bv.y + h.y * h.y);
+                const R m0 = fast_mag(bv.x, h.x);
+                const R m1 = fast_mag(bv.y, h.y);
                 const unsigned t = 2u * (unsigned)n + (unsigned)c0;
                 const int u = (int)__umulhi(t, dmagic);
                 const int pp = (int)t - u * D;
@@ -604,8 +607,8 @@ __global__ void __launch_bounds__(kThreads * G, (M >= 8192 || M <= 2048) ? 1 : (
                     const int n = m + 256 * k;
                     const V h = v[out_slot<16>(k)];
                     const V bv = __ldg(bsrc + n);
-                    const R m0 = fast_sqrt(bv.x * bv.x + h.x * h.x);
-                    const R m1 = fast_sqrt(bv.y * bv.y + h.y * h.y);
+                    const R m0 = fast_mag(bv.x, h.x);
+                    const R m1 = fast_mag(bv.y, h.y);
                     return V{2 * n < Li ? m0 : (R)0, 2 * n + 1 < Li ? m1 : (R)0};
                 };
 #pragma unroll
@@ -868,8 +871,8 @@ __global__ void __launch_bounds__(kThreads, SNB_ENV_MINB) k_envelope_pair2048(En
                 const int n = u + 128 * out_slot<16>(r);
                 const V hv = v[r];
                 const V bv = __ldg(src + n);
-                const R m0 = fast_sqrt(bv.x * bv.x + hv.x * hv.x);
-                const R m1 = fast_sqrt(bv.y * bv.y + hv.y * hv.y);
+                const R m0 = fast_mag(bv.x, hv.x);
+                const R m1 = fast_mag(bv.y, hv.y);
                 const unsigned tt = 2u * (unsigned)n + (unsigned)c0;
                 const int uu = (int)__umulhi(tt, dmagic);
                 const int pp = (int)tt - uu * D;
@@ -1007,8 +1010,8 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_envelope_split8192(EnvArgs 
                 const int n = j + 256 * r + 4096 * h;
                 const V hv = zz[r];
                 const V bv = __ldg(src + n);
-                const R m0 = fast_sqrt(bv.x * bv.x + hv.x * hv.x);
-                const R m1 = fast_sqrt(bv.y * bv.y + hv.y * hv.y);
+                const R m0 = fast_mag(bv.x, hv.x);
+                const R m1 = fast_mag(bv.y, hv.y);
                 const unsigned tt = 2u * (unsigned)n + (unsigned)c0;
                 const int uu = (int)__umulhi(tt, dmagic);
                 const int pp = (int)tt - uu * D;
