@@ -126,6 +126,22 @@ class _Measurement(C.Structure):
     ]
 
 
+_MEAS_DTYPE = None
+
+
+def _measurement_dtype():
+    """numpy dtype with _Measurement's field offsets (pointers as uint64)."""
+    global _MEAS_DTYPE
+    if _MEAS_DTYPE is None:
+        conv = {C.c_uint32: np.uint32, C.c_uint64: np.uint64, C.c_uint16: np.uint16, C.c_double: np.float64}
+        names = [n for n, _ in _Measurement._fields_]
+        _MEAS_DTYPE = np.dtype({"names": names,
+                                "formats": [conv.get(t, np.uint64) for _, t in _Measurement._fields_],
+                                "offsets": [getattr(_Measurement, n).offset for n in names],
+                                "itemsize": C.sizeof(_Measurement)})
+    return _MEAS_DTYPE
+
+
 class _Dims(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "frames", "demod_samples", "mf_samples", "range_bins", "n_directions", "ref_len",
@@ -619,12 +635,17 @@ class Workspace:
         """Fast host path for B equal-sized captures already packed as
         (B, packed_bytes) uint8 (e.g. pinned); out (B, n_dirs, bins) f32."""
         B = packed.shape[0]
-        structs = (_Measurement * B)()
-        base = packed.ctypes.data
-        for i in range(B):
-            structs[i] = _Measurement(1, 0, i, 32, self.frames, self._cfg.pdm_rate,
-                                      C.cast(base + i * self.packed_bytes, C.POINTER(C.c_uint8)),
-                                      self.packed_bytes)
+        # the sn_raw_measurement array built column-wise in numpy (a Python
+        # loop over ctypes structs cost 0.3 ms per 128 captures)
+        a = np.zeros(B, _measurement_dtype())
+        a["sensor_serial"] = 1
+        a["seq"] = np.arange(B, dtype=np.uint64)
+        a["channels"] = 32
+        a["frames"] = self.frames
+        a["pdm_rate"] = self._cfg.pdm_rate
+        a["packed"] = np.uint64(packed.ctypes.data) + np.arange(B, dtype=np.uint64) * np.uint64(packed.strides[0])
+        a["packed_len"] = self.packed_bytes
+        structs = (_Measurement * B).from_buffer(a)
         _check(lib().sn_workspace_process_batch(self._h, structs, B, out.ctypes.data))
         return out
 

@@ -266,8 +266,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
+#ifdef SNB_TC_EXP_TIMES
+// developer diagnostic: per-CTA busy time (globaltimer ns) summed over
+// launches, and per-CTA MMA-warp time blocked on slots / windows
+__device__ unsigned long long g_tc_times[4 * 1024];
+#endif
+
 template <int TN>
 __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const __grid_constant__ TcSched sched) {
+#ifdef SNB_TC_EXP_TIMES
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
     constexpr int kSlots = slots_for<TN>();
     constexpr int kWin = win_for(TN);
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -300,7 +310,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     const int per_cb = a.batch * a.ntiles;
+#ifdef SNB_TC_EXP_REVERSE
+    // timing experiment: CTA k runs the range of CTA grid - 1 - k
+    const int t_beg = sched.start[gridDim.x - 1 - blockIdx.x], t_end = sched.start[gridDim.x - blockIdx.x];
+#else
     const int t_beg = sched.start[blockIdx.x], t_end = sched.start[blockIdx.x + 1];
+#endif
     const int ntile = t_end - t_beg;
 
     if (warp == kEpiWarps) {
@@ -546,6 +561,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
             }
         }
     }
+#ifdef SNB_TC_EXP_TIMES
+    if (warp == kEpiWarps) {
+        unsigned long long t_fin;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_fin));
+        unsigned sr = 0, sw = 0;
+        for (int t = t_beg + lane; t < t_end; t += 32) {
+            const int c = t / per_cb;
+            sr += (unsigned)a.R[c];
+            sw += (t == t_beg || (t - 1) / per_cb != c) ? 1u : 0u;
+        }
+        sr = __reduce_add_sync(0xffffffffu, sr);
+        sw = __reduce_add_sync(0xffffffffu, sw);
+        if (lane == 0) {
+            atomicAdd(&g_tc_times[4 * blockIdx.x], t_fin - t_start);
+            atomicAdd(&g_tc_times[4 * blockIdx.x + 1], 1ull);
+            atomicAdd(&g_tc_times[4 * blockIdx.x + 3], (unsigned long long)sr);
+            atomicAdd(&g_tc_times[2048 + 2 * blockIdx.x], (unsigned long long)(t_end - t_beg));
+            atomicAdd(&g_tc_times[2048 + 2 * blockIdx.x + 1], (unsigned long long)sw);
+        }
+        __syncwarp();
+    }
+    if (tid == 0) {
+        unsigned long long t_fin;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_fin));
+        atomicAdd(&g_tc_times[4 * blockIdx.x + 2], t_fin - t_start);
+    }
+    __syncwarp();
+#endif
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     if (warp == 0) {
@@ -579,3 +622,10 @@ cudaError_t launch_beamform_tc(const TcArgs& a, const TcSched& sched, int grid, 
 }
 
 } // namespace snb
+
+#ifdef SNB_TC_EXP_TIMES
+extern "C" int sn_debug_tc_times(unsigned long long* out, int n) {
+    if (cudaMemcpyFromSymbol(out, snb::g_tc_times, sizeof(unsigned long long) * (size_t)n) != cudaSuccess) return -1;
+    return 0;
+}
+#endif

@@ -313,3 +313,26 @@ def test_hot_kernels_register_budget(sn):
         hits = [v for k, v in usage.items() if k.startswith(prefix)]
         assert hits, prefix
         assert all(st <= lim for _, st in hits), (prefix, hits)
+
+
+def test_measurement_dtype_matches_ctypes_layout(sn):
+    """process_packed_host fills sn_raw_measurement structs column-wise via a
+    numpy dtype built from the ctypes field offsets: same bytes as ctypes."""
+    import ctypes as C
+    M = sn._Measurement
+    dt = sn._measurement_dtype()
+    assert dt.itemsize == C.sizeof(M)
+    buf = np.zeros(4, dt)
+    data = np.zeros((4, 16), np.uint8)
+    buf["sensor_serial"] = 7
+    buf["timestamp_us"] = 123456789
+    buf["seq"] = np.arange(4)
+    buf["channels"] = 32
+    buf["frames"] = 144800
+    buf["pdm_rate"] = 4.5e6
+    buf["packed"] = np.uint64(data.ctypes.data) + np.arange(4, dtype=np.uint64) * np.uint64(16)
+    buf["packed_len"] = 16
+    s = (M * 4).from_buffer(buf)
+    for i in range(4):
+        ref = M(7, 123456789, i, 32, 144800, 4.5e6, C.cast(data.ctypes.data + 16 * i, C.POINTER(C.c_uint8)), 16)
+        assert bytes(s[i]) == bytes(ref)
