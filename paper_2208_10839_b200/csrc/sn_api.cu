@@ -680,14 +680,21 @@ struct sn_workspace {
     }
 
     // contiguous per-CTA tile ranges of equal estimated work. A tile costs
-    // the larger of its MMA time (R_c units of six MMAs) and the epilogue's
-    // drain + recombination of six accumulators (independent of R_c,
-    // kTcEpiUnits of the same units), plus a small fixed part
+    // the larger of its MMA time (R_c units of six MMAs) and an epilogue
+    // floor (SNB_TC_EPI_UNITS), plus a fixed part. Per-CTA busy times
+    // (scripts/tc_times.py, globaltimer per CTA) showed the fixed part
+    // dominating: ~3.8 us + 0.06 us x R_c per tile, i.e. R_c + ~60 units, and
+    // the round-1 model max(R_c, 20) + 2 leaving a max/mean CTA time of 1.08.
+    // A/B (beamform stage vs max(R, 20) + 2, sweep grids, min of 2 runs):
+    // R + 20: hemi3000 0.97, box1850 0.93, fib10k 0.98-1.00, fib30k 1.04;
+    // R + 30: 0.96-0.98, 0.95-0.96, 0.95-0.98, 1.02-1.03;
+    // R + 40: 0.96, 0.97-0.99, 0.93-0.97, 1.015 (1- and 2-cluster grids
+    // within run-to-run noise)
 #ifndef SNB_TC_EPI_UNITS
-#define SNB_TC_EPI_UNITS 20 // A/B on hemisphere3000 (beamform ms): 8: 1.347, 14: 1.390, 16: 1.322, 20: 1.287, 24: 1.287
+#define SNB_TC_EPI_UNITS 0
 #endif
 #ifndef SNB_TC_FIXED_UNITS
-#define SNB_TC_FIXED_UNITS 2
+#define SNB_TC_FIXED_UNITS 30
 #endif
     static double tc_tile_cost(int R) {
         return std::max<double>(R, SNB_TC_EPI_UNITS) + SNB_TC_FIXED_UNITS;
