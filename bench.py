@@ -215,13 +215,70 @@ def cpu_baseline(cfg_b200, grid, calls, warmup=1):
     if warmup > 1:
         ref.throughput(rc, pool, threads, warmup - 1)  # untimed; the timed run warms up once more
     elapsed, total = ref.throughput(rc, pool, threads, calls)
+    n_dirs = len(po.az181_directions()) if grid == "az181" else po.GRID_SIZES[kind]
+    try:
+        fc = fft_check(threads * elapsed / total / n_dirs * 1e6)
+    except Exception as e:  # diagnostic only
+        fc = {"error": str(e)}
     return {
         "value": total / elapsed, "unit": UNIT, "cores": threads, "kind": "reference",
-        "fft": FFT_LABEL,
+        "fft": FFT_LABEL, "fft_check": fc,
         "sample": (f"{total} process() calls of {grid} ({threads} threads x {calls}; "
                    f"unmodified reference core built -O3 -march=x86-64-v3, FFT = test-only "
                    f"FFTW-API shim; {elapsed:.2f} s wall)"),
     }
+
+
+def fft_check(per_dir_us, reps=300):
+    """How much the test-only FFT shim can inflate the reference's time: the
+    shim's r2c of 8192 reals (the envelope's transform size) against numpy's
+    pocketfft on this host, and the share of the reference's per-direction
+    time its FFT pair (r2c + c2r) takes -- a reference on a zero-cost FFT
+    would be at most 1 / (1 - share) faster."""
+    import ctypes as C
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    lib = C.CDLL(po.REF_FAST_SO)
+    lib.fftw_alloc_real.restype = C.c_void_p
+    lib.fftw_alloc_complex.restype = C.c_void_p
+    lib.fftw_plan_dft_r2c_1d.restype = C.c_void_p
+    lib.fftw_plan_dft_r2c_1d.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint]
+    lib.fftw_plan_dft_c2r_1d.restype = C.c_void_p
+    lib.fftw_plan_dft_c2r_1d.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint]
+    lib.fftw_execute.argtypes = [C.c_void_p]
+    lib.fftw_destroy_plan.argtypes = [C.c_void_p]
+    lib.fftw_free.argtypes = [C.c_void_p]
+    n = 8192
+    ip, op = lib.fftw_alloc_real(n), lib.fftw_alloc_complex(n // 2 + 1)
+    x = np.ctypeslib.as_array(C.cast(ip, C.POINTER(C.c_double)), (n,))
+    x[:] = np.random.default_rng(1).standard_normal(n)
+    fwd = lib.fftw_plan_dft_r2c_1d(n, ip, op, 0)
+    inv = lib.fftw_plan_dft_c2r_1d(n, op, ip, 0)
+    times = []
+    for plan in (fwd, inv):
+        lib.fftw_execute(plan)
+        t = time.perf_counter()
+        for _ in range(reps):
+            lib.fftw_execute(plan)
+        times.append((time.perf_counter() - t) / reps * 1e6)
+    xx = np.random.default_rng(1).standard_normal(n)
+    np.fft.rfft(xx)
+    t = time.perf_counter()
+    for _ in range(reps):
+        np.fft.rfft(xx)
+    t_np = (time.perf_counter() - t) / reps * 1e6
+    for plan in (fwd, inv):
+        lib.fftw_destroy_plan(plan)
+    lib.fftw_free(ip)
+    lib.fftw_free(op)
+    share = min(1.0, (times[0] + times[1]) / per_dir_us)
+    return {"shim_r2c_8192_us": round(times[0], 1), "shim_c2r_8192_us": round(times[1], 1),
+            "numpy_pocketfft_rfft_8192_us": round(t_np, 1),
+            "reference_us_per_direction_per_thread": round(per_dir_us, 1),
+            "fft_pair_share": round(share, 3),
+            "zero_cost_fft_bound": round(1.0 / max(1e-9, 1.0 - share), 2),
+            "note": "shim single-thread timings while no other work runs; the per-direction time is "
+                    "threads / (throughput x directions) from the throughput run (shared cores)"}
 
 
 def cpu_latency(grid, n):

@@ -302,7 +302,9 @@ def test_hot_kernels_register_budget(sn):
             usage[cur] = (int(m.group(1)), int(m.group(2)))
     limits = {  # mangled name prefix -> max stack bytes
         "_ZN3snb10k_envelopeIdLi2ELi4096ELb1E": 16,   # default FP64 envelope (N = 8192, FFT FIR)
-        "_ZN3snb10k_envelopeIfLi3ELi4096ELb1E": 0,
+        # FP32 (3 groups at 80 registers): the fused first FIR pass costs a
+        # 40 B frame and is still faster (envelope 1.87 -> 1.72 ms)
+        "_ZN3snb10k_envelopeIfLi3ELi4096ELb1E": 48,
         "_ZN3snb19k_envelope_pair2048IdE": 0,           # 1.5 m window
         "_ZN3snb20k_envelope_split8192IdE": 32,         # 10 m window
         "_ZN3snb13k_beamform_tcILi96E": 64,             # tensor-core delay-and-sum
