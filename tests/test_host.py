@@ -338,3 +338,32 @@ def test_measurement_dtype_matches_ctypes_layout(sn):
     for i in range(4):
         ref = M(7, 123456789, i, 32, 144800, 4.5e6, C.cast(data.ctypes.data + 16 * i, C.POINTER(C.c_uint8)), 16)
         assert bytes(s[i]) == bytes(ref)
+
+
+@pytest.mark.parametrize("c0", [1, 63, 223, 255, 257, 321, 511])
+def test_fused_sink_covers_fir_layout_once(c0):
+    """k_envelope's fused sink (kernels.cu, FFT FIR): thread m of the last
+    inverse pass holds samples t_k = 2m + c0 + 512k (k = 0..15) and runs the
+    FIR's radix-3 butterflies over (t, t + 2560, t + 5120) for the five t_k in
+    [0, 2560) -- k = 0..4 if t_0 < 512, else k = -1..3 (t_-1 < c0: a zero
+    sample). Every slot (sequence a, position u < 768) of the layout must be
+    written exactly once, and each butterfly's members must be the slots
+    u, u + 256, u + 512 of one sequence."""
+    seen = np.zeros((5, 768), np.int32)
+    for m in range(256):
+        t0 = 2 * m + c0
+        hi = t0 >= 512
+        for j in range(5):
+            ks = (j, j + 5, j + 10) if j < 4 else ((-1, 4, 9) if hi else (4, 9, 14))
+            t = t0 - 512 if (j == 4 and hi) else t0 + 512 * j
+            assert 0 <= t < 2560 and t % 2 == 1
+            for n1, k in enumerate(ks):
+                tk = t0 + 512 * k
+                assert tk == t + 2560 * n1            # member n1 of the butterfly
+                assert k <= 14                        # output k = 15 is never needed
+                u, sa = tk // 10, (tk % 10 - 1) // 2
+                assert u == t // 10 + 256 * n1 and sa == (t % 10 - 1) // 2
+                if k < 0:
+                    assert tk < c0                    # the zero sample below the window
+                seen[sa, u] += 1
+    assert (seen == 1).all()
