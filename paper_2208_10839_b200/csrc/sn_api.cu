@@ -154,8 +154,11 @@ struct sn_workspace {
             v.assign(c, 1);
             return v;
         }
+#ifndef SNB_ENV_SUB
+#define SNB_ENV_SUB 2 // captures per envelope sub-chunk (the last one: 1)
+#endif
         uint64_t rest = c - 1;
-        const uint64_t n = std::min<uint64_t>((rest + 1) / 2, kMaxChunks - 1);
+        const uint64_t n = std::min<uint64_t>((rest + SNB_ENV_SUB - 1) / SNB_ENV_SUB, kMaxChunks - 1);
         for (uint64_t j = 0; j < n; ++j) v.push_back(rest / n + (j < rest % n ? 1 : 0));
         v.push_back(1);
         return v;
@@ -1025,13 +1028,23 @@ struct sn_workspace {
             const uint64_t c = std::min(max_batch, count - done);
             const int half = (int)(blk & 1);
             float* d_en = d_energy + (uint64_t)half * max_batch * energy_per;
-            // captures uploaded in up to 4 parts (copy stream), the front end
-            // of part p running while part p + 1 is on the bus; the
-            // beamformer for the whole block; then the envelope in chunks whose
-            // energyscapes are downloaded (D2H stream) while the next chunk
-            // computes: only the first part's upload and the last chunk's
-            // download are exposed
-            const uint64_t parts = std::min<uint64_t>(c, 4);
+            // the first block's captures uploaded in up to 4 parts (copy
+            // stream), the front end of part p running while part p + 1 is on
+            // the bus; the beamformer for the whole block; then the envelope
+            // in chunks whose energyscapes are downloaded (D2H stream) while
+            // the next chunk computes: only the first part's upload and the
+            // last chunk's download are exposed. Later blocks upload in one
+            // part: their upload runs under the previous block's envelope,
+            // and a front end split in 4 costs more than it hides (e2e A/B,
+            // 128 captures per call: 4 parts every block 3,685 /s, 2 parts
+            // 3,759, 1 part 3,786)
+#ifndef SNB_E2E_PARTS
+#define SNB_E2E_PARTS 4
+#endif
+#ifndef SNB_E2E_PARTS_LATER
+#define SNB_E2E_PARTS_LATER 1
+#endif
+            const uint64_t parts = std::min<uint64_t>(c, blk == 0 ? SNB_E2E_PARTS : SNB_E2E_PARTS_LATER);
             if (blk > 0) ck(cudaStreamWaitEvent(s_h2d, ev_front, 0), "wait"); // d_packed consumed
             uint64_t p0 = 0;
             for (uint64_t p = 0; p < parts; ++p) {
