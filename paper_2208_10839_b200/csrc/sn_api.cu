@@ -582,15 +582,18 @@ struct sn_workspace {
         in_frame_len = 36 + 38 + packed_bytes + 4;
         in_frame_stride = (in_frame_len + 15) & ~uint64_t(15);
         const uint64_t B = max_batch;
-        d_frames_out = dmalloc<uint8_t>(B * img_frame_stride, n);
+        // output frames, host-side ids and CRC verdicts in two halves: the
+        // blocks of one process_frames call alternate (block j + 1 is
+        // enqueued while block j's frames download)
+        d_frames_out = dmalloc<uint8_t>(2 * B * img_frame_stride, n);
         d_frames_in = dmalloc<uint8_t>(B * in_frame_stride, n);
         d_ids = dmalloc<FrameIds>(B, n);
         d_crc_acc = dmalloc<uint32_t>(2 * B, n);
         d_crc_ok = dmalloc<int32_t>(B, n);
         ck(cudaMallocHost(&h_frames_out, B * img_frame_len), "cudaMallocHost");
         ck(cudaMallocHost(&h_frames_in, B * in_frame_len), "cudaMallocHost");
-        ck(cudaMallocHost(&h_ids, B * sizeof(FrameIds)), "cudaMallocHost");
-        ck(cudaMallocHost(&h_crc_ok, B * sizeof(int32_t)), "cudaMallocHost");
+        ck(cudaMallocHost(&h_ids, 2 * B * sizeof(FrameIds)), "cudaMallocHost");
+        ck(cudaMallocHost(&h_crc_ok, 2 * B * sizeof(int32_t)), "cudaMallocHost");
     }
     CrcTables crc_tables() const { return CrcTables{d_crc_slice, d_crc_shift, d_crc_lane}; }
 
@@ -1118,68 +1121,28 @@ struct sn_workspace {
         const Sizes& z = plan.sz;
         const bool out_pinned = is_pinned(out);
         after_last(stream);
+        after_last(s_h2d);
+        after_last(s_d2h);
+        // Blocks of up to max_batch accepted frames. A block whose frames are
+        // all page-locked and whose output slots are consecutive in a
+        // page-locked `out` (frames DMA'd both ways, no staging) is left in
+        // flight: the next block is enqueued behind it (its upload on the copy
+        // stream under this block's envelope, its front end after this
+        // block's beams), and its verdicts are read once its downloads are
+        // done; the two halves of the output frames / ids / verdicts
+        // alternate. Any other block is finished before the next one starts.
         std::vector<uint64_t> batch;
         batch.reserve(max_batch);
-        auto flush = [&]() {
-            if (batch.empty()) return;
-            const uint64_t c = batch.size();
-            for (uint64_t i = 0; i < c; ++i) {
-                const uint8_t* f = frames[batch[i]];
-                if (is_pinned(f)) {
-                    ck(cudaMemcpyAsync(d_frames_in + i * in_frame_stride, f, in_frame_len, cudaMemcpyHostToDevice,
-                                       stream), "H2D frame");
-                } else {
-                    std::memcpy(h_frames_in + i * in_frame_len, f, in_frame_len);
-                    ck(cudaMemcpyAsync(d_frames_in + i * in_frame_stride, h_frames_in + i * in_frame_len,
-                                       in_frame_len, cudaMemcpyHostToDevice, stream), "H2D frame");
-                }
-                FrameIds id{};
-                std::memcpy(&id.serial, f + 36, 4);
-                std::memcpy(&id.ts, f + 40, 8);
-                std::memcpy(&id.seq, f + 48, 8);
-                h_ids[i] = id;
-            }
-            ck(cudaMemcpyAsync(d_ids, h_ids, c * sizeof(FrameIds), cudaMemcpyHostToDevice, stream), "H2D ids");
-            ck(cudaMemsetAsync(d_crc_acc, 0, 2 * max_batch * sizeof(uint32_t), stream), "memset");
-            const CrcTables ct = crc_tables();
-            const uint64_t nin = in_frame_len - 4;
-            launch_crc_partial(d_frames_in, in_frame_stride, nin, c, ct, d_crc_acc, stream);
-            launch_crc_finalize(d_crc_acc, crc_init_term(h_crc_shift.data(), nin), c, d_frames_in, in_frame_stride,
-                                nin, false, d_crc_ok, stream);
-            ck(cudaMemcpy2DAsync(d_packed, packed_bytes, d_frames_in + 74, in_frame_stride, packed_bytes, c,
-                                 cudaMemcpyDeviceToDevice, stream), "D2D packed");
-            enqueue_front(d_packed, 0, c, stream);
-            // envelope + frame encode in chunks; each chunk's frames download
-            // (D2H stream) while the next chunk computes. D2H straight into the
-            // caller's slots when they are page-locked and consecutive.
-            const bool direct = out_pinned && batch.back() - batch.front() == c - 1;
-            const uint64_t nout = img_frame_len - 4;
-            const uint32_t kout = crc_init_term(h_crc_shift.data(), nout);
-            enqueue_per_direction(c, [&](uint64_t off, uint64_t k, cudaStream_t cs, cudaEvent_t ed) {
-                ImageFrameArgs ia{d_energy + off * energy_per, d_img_tpl, d_ids + off,
-                                  d_frames_out + off * img_frame_stride, d_crc_acc + max_batch + off, energy_per,
-                                  img_tpl_len, img_frame_len, img_frame_stride};
-                launch_encode_image_frames(ia, k, ct, cs);
-                launch_crc_finalize(d_crc_acc + max_batch + off, kout, k, d_frames_out + off * img_frame_stride,
-                                    img_frame_stride, nout, true, nullptr, cs);
-                ck(cudaEventRecord(ed, cs), "event");
-                ck(cudaStreamWaitEvent(s_d2h, ed, 0), "wait");
-                uint8_t* dst = direct ? out + (batch.front() + off) * slot : h_frames_out + off * img_frame_len;
-                const uint64_t dpitch = direct ? slot : img_frame_len;
-                for (uint64_t i = 0; i < k; ++i) {
-                    ck(cudaMemcpyAsync(dst + i * dpitch, d_frames_out + (off + i) * img_frame_stride, img_frame_len,
-                                       cudaMemcpyDeviceToHost, s_d2h), "D2H frame");
-                }
-                return uint64_t{2};
-            });
-            ck(cudaGetLastError(), "frame kernels");
-            ck(cudaStreamSynchronize(s_d2h), "frames sync");
-            ck(cudaMemcpyAsync(h_crc_ok, d_crc_ok, c * sizeof(int32_t), cudaMemcpyDeviceToHost, stream), "D2H ok");
-            ck(cudaStreamSynchronize(stream), "frames sync");
-            for (uint64_t i = 0; i < c; ++i) {
-                const uint64_t k = batch[i];
-                if (h_crc_ok[i]) {
-                    if (!direct) std::memcpy(out + k * slot, h_frames_out + i * img_frame_len, img_frame_len);
+        std::vector<uint64_t> pend[2];
+        uint64_t blk = 0;
+        auto finish = [&](int half, bool staged) {
+            if (pend[half].empty()) return;
+            ck(cudaEventSynchronize(ev_d2h[half]), "frames sync");
+            const int32_t* ok = h_crc_ok + (uint64_t)half * max_batch;
+            for (uint64_t i = 0; i < pend[half].size(); ++i) {
+                const uint64_t k = pend[half][i];
+                if (ok[i]) {
+                    if (staged) std::memcpy(out + k * slot, h_frames_out + i * img_frame_len, img_frame_len);
                     out_lens[k] = img_frame_len;
                     status[k] = SN_OK;
                 } else {
@@ -1187,6 +1150,84 @@ struct sn_workspace {
                     status[k] = SN_ERR_IO;
                 }
             }
+            pend[half].clear();
+        };
+        auto flush = [&]() {
+            if (batch.empty()) return;
+            const uint64_t c = batch.size();
+            const int half = (int)(blk & 1);
+            finish(half, false); // block blk - 2 (pipelined: no staging)
+            bool in_pinned = true;
+            for (uint64_t i = 0; i < c && in_pinned; ++i) in_pinned = is_pinned(frames[batch[i]]);
+            const bool direct = out_pinned && batch.back() - batch.front() == c - 1;
+            const bool pipelined = direct && in_pinned;
+            if (!pipelined) finish(half ^ 1, false); // staging buffers are shared: drain first
+            FrameIds* hid = h_ids + (uint64_t)half * max_batch;
+            uint8_t* dfo = d_frames_out + (uint64_t)half * max_batch * img_frame_stride;
+            // the input frames (and d_packed) are free once the previous
+            // block's front end has run
+            if (blk > 0) ck(cudaStreamWaitEvent(s_h2d, ev_front, 0), "wait");
+            for (uint64_t i = 0; i < c; ++i) {
+                const uint8_t* f = frames[batch[i]];
+                if (in_pinned) {
+                    ck(cudaMemcpyAsync(d_frames_in + i * in_frame_stride, f, in_frame_len, cudaMemcpyHostToDevice,
+                                       s_h2d), "H2D frame");
+                } else {
+                    std::memcpy(h_frames_in + i * in_frame_len, f, in_frame_len);
+                    ck(cudaMemcpyAsync(d_frames_in + i * in_frame_stride, h_frames_in + i * in_frame_len,
+                                       in_frame_len, cudaMemcpyHostToDevice, s_h2d), "H2D frame");
+                }
+                FrameIds id{};
+                std::memcpy(&id.serial, f + 36, 4);
+                std::memcpy(&id.ts, f + 40, 8);
+                std::memcpy(&id.seq, f + 48, 8);
+                hid[i] = id;
+            }
+            ck(cudaEventRecord(ev_in[0], s_h2d), "event");
+            ck(cudaStreamWaitEvent(stream, ev_in[0], 0), "wait");
+            ck(cudaMemcpyAsync(d_ids, hid, c * sizeof(FrameIds), cudaMemcpyHostToDevice, stream), "H2D ids");
+            ck(cudaMemsetAsync(d_crc_acc, 0, 2 * max_batch * sizeof(uint32_t), stream), "memset");
+            const CrcTables ct = crc_tables();
+            const uint64_t nin = in_frame_len - 4;
+            launch_crc_partial(d_frames_in, in_frame_stride, nin, c, ct, d_crc_acc, stream);
+            launch_crc_finalize(d_crc_acc, crc_init_term(h_crc_shift.data(), nin), c, d_frames_in, in_frame_stride,
+                                nin, false, d_crc_ok, stream);
+            ck(cudaMemcpyAsync(h_crc_ok + (uint64_t)half * max_batch, d_crc_ok, c * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, stream), "D2H ok");
+            ck(cudaMemcpy2DAsync(d_packed, packed_bytes, d_frames_in + 74, in_frame_stride, packed_bytes, c,
+                                 cudaMemcpyDeviceToDevice, stream), "D2D packed");
+            enqueue_front(d_packed, 0, c, stream);
+            ck(cudaEventRecord(ev_front, stream), "event");
+            ck(cudaEventRecord(ev_beams, stream), "event");
+            ck(cudaStreamWaitEvent(s_d2h, ev_beams, 0), "wait"); // the verdicts' download precedes ev_d2h
+            // envelope + frame encode in chunks; each chunk's frames download
+            // (D2H stream) while the next chunk computes. D2H straight into the
+            // caller's slots when they are page-locked and consecutive. The
+            // envelope of this half waits for block blk - 2's downloads.
+            const uint64_t nout = img_frame_len - 4;
+            const uint32_t kout = crc_init_term(h_crc_shift.data(), nout);
+            enqueue_per_direction(c, [&](uint64_t off, uint64_t k, cudaStream_t cs, cudaEvent_t ed) {
+                ImageFrameArgs ia{d_energy + off * energy_per, d_img_tpl, d_ids + off,
+                                  dfo + off * img_frame_stride, d_crc_acc + max_batch + off, energy_per,
+                                  img_tpl_len, img_frame_len, img_frame_stride};
+                launch_encode_image_frames(ia, k, ct, cs);
+                launch_crc_finalize(d_crc_acc + max_batch + off, kout, k, dfo + off * img_frame_stride,
+                                    img_frame_stride, nout, true, nullptr, cs);
+                ck(cudaEventRecord(ed, cs), "event");
+                ck(cudaStreamWaitEvent(s_d2h, ed, 0), "wait");
+                uint8_t* dst = direct ? out + (batch.front() + off) * slot : h_frames_out + off * img_frame_len;
+                const uint64_t dpitch = direct ? slot : img_frame_len;
+                for (uint64_t i = 0; i < k; ++i) {
+                    ck(cudaMemcpyAsync(dst + i * dpitch, dfo + (off + i) * img_frame_stride, img_frame_len,
+                                       cudaMemcpyDeviceToHost, s_d2h), "D2H frame");
+                }
+                return uint64_t{2};
+            }, blk >= 2 ? ev_d2h[half] : nullptr);
+            ck(cudaEventRecord(ev_d2h[half], s_d2h), "event");
+            ck(cudaGetLastError(), "frame kernels");
+            pend[half] = batch;
+            if (!pipelined) finish(half, !direct);
+            ++blk;
             batch.clear();
         };
         for (uint64_t k = 0; k < count; ++k) {
@@ -1250,7 +1291,9 @@ struct sn_workspace {
             if (batch.size() == max_batch) flush();
         }
         flush();
-        mark_last(stream);
+        if (blk >= 2) finish((int)(blk & 1), false); // block blk - 2
+        if (blk >= 1) finish((int)((blk - 1) & 1), false);
+        mark_last(stream); // every block was waited for above
         (void)z;
     }
 

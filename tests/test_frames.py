@@ -174,3 +174,53 @@ def test_central_pool_fifo_and_worker_transparency(sn, po, ref):
             continue
         want = rws.process_frame(f)
         assert status == 0 and len(got) == len(want) and got[:36] == want[:36]
+
+
+@pytest.mark.gpu
+def test_process_frames_pipelined_blocks_match_unpipelined(sn):
+    """Page-locked frames in and a page-locked output: the blocks of one call
+    pipeline into each other (alternating output halves, verdicts read when a
+    block's downloads are done). Byte-identical frames and statuses against the
+    pageable (block-synchronous) path, with a CRC-corrupted frame (discarded;
+    its block's output slots are no longer consecutive, so that block is
+    staged) and a mix of page-locked and pageable inputs."""
+    import ctypes as C
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = sn.default_pipeline_config(sn.GridKind.horizontal90)
+    ws = sn.Workspace(cfg, device=0, max_batch=3)
+    n = 13
+    frames = []
+    for i in range(n):
+        m = sn.synthesize_measurement(cfg, sn.Scene([sn.Reflector(0.5 + 0.1 * i, 0.2, 0.0, 0.8)], 0.01, 70 + i),
+                                      serial=1 + i % 4, timestamp_us=500 * i, seq=i)
+        frames.append(bytearray(sn.measurement_frame(m)))
+    frames[4][1000] ^= 0x40  # payload corrupted: CRC mismatch, discarded
+    frames = [bytes(f) for f in frames]
+    want = ws.process_frames(frames)  # pageable: every block finished before the next
+    assert [s for s, _ in want].count(0) == n - 1 and want[4][0] != 0
+
+    slot = ws.image_frame_bytes
+    flen = len(frames[0])
+    L = sn.lib()
+
+    def run(pinned_mask):
+        pin = torch.empty((n, flen), dtype=torch.uint8).pin_memory()
+        pg = np.empty((n, flen), np.uint8)
+        for i, f in enumerate(frames):
+            (pin.numpy() if pinned_mask[i] else pg)[i] = np.frombuffer(f, np.uint8)
+        ptrs = (C.c_void_p * n)(*[(pin.numpy() if pinned_mask[i] else pg)[i].ctypes.data for i in range(n)])
+        lens = (C.c_uint64 * n)(*([flen] * n))
+        out = torch.zeros((n, slot), dtype=torch.uint8).pin_memory()
+        olen, st = (C.c_uint64 * n)(), (C.c_int32 * n)()
+        assert L.sn_workspace_process_frames(ws._h, ptrs, lens, n, out.numpy().ctypes.data, slot, olen, st) == 0
+        o = out.numpy()
+        return [(int(st[i]), o[i, :olen[i]].tobytes()) for i in range(n)]
+
+    for mask in ([True] * n, [i < 6 for i in range(n)], [i % 5 != 2 for i in range(n)]):
+        for _ in range(2):  # twice: the second call starts on the halves the first left
+            got = run(mask)
+            for i in range(n):
+                assert got[i][0] == want[i][0], (mask, i)
+                assert got[i][1] == want[i][1], (mask, i)
