@@ -74,6 +74,29 @@ __device__ __forceinline__ uint32_t lane_to_segment_end(const uint32_t* s_lane, 
     return r;
 }
 
+// The warp's segment CRC (lane chunks already moved to the segment end,
+// XOR-reduced here) moved on to the string end. A full segment s with the
+// per-length table: lane b holds column b of A_{n - 4096 (s + 1)} (loaded
+// before the CRC loop), the product is a masked XOR reduction across the warp;
+// otherwise lane 0 runs the A_{2^k} chain. Lane 0 returns the result.
+__device__ __forceinline__ uint32_t segment_to_end(const CrcTables& ct, bool full, uint64_t w0, uint64_t n,
+                                                   uint32_t c, uint32_t seg_col, int l) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
+    if (full && ct.seg) {
+        uint32_t r = (c >> l) & 1u ? seg_col : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r ^= __shfl_xor_sync(0xffffffffu, r, o);
+        return r;
+    }
+    if (l == 0 && full) c = crc_shift(ct.shift, c, n - 4 * (w0 + kSegWords));
+    return c;
+}
+
+__device__ __forceinline__ uint32_t seg_column(const CrcTables& ct, uint64_t w0, uint64_t nw, int l) {
+    return ct.seg && w0 + kSegWords <= nw ? __ldg(ct.seg + 32 * (w0 / kSegWords) + l) : 0u;
+}
+
 __global__ void __launch_bounds__(32 * kEncWarps) k_crc_partial(const uint8_t* base, uint64_t stride, uint64_t n,
                                                                 CrcTables ct, uint32_t* acc) {
     __shared__ uint32_t s_tab[1024];
@@ -86,6 +109,7 @@ __global__ void __launch_bounds__(32 * kEncWarps) k_crc_partial(const uint8_t* b
     const uint64_t nw = n / 4; // full words; then n % 4 tail bytes
     const uint64_t w0 = ((uint64_t)blockIdx.x * kEncWarps + warp) * kSegWords;
     if (w0 > nw || (w0 == nw && (n & 3) == 0)) return;
+    const uint32_t seg_col = seg_column(ct, w0, nw, l);
     const uint8_t* p = base + (size_t)f * stride;
     const uint32_t* pw = reinterpret_cast<const uint32_t*>(p);
     uint32_t* sw = s_w[warp];
@@ -114,12 +138,8 @@ __global__ void __launch_bounds__(32 * kEncWarps) k_crc_partial(const uint8_t* b
         const uint64_t end = cw0 + 32 <= nw ? 4 * (cw0 + 32) : n;
         c = cw0 <= nw ? crc_shift(ct.shift, c, n - end) : 0u;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
-    if (l == 0) {
-        if (full) c = crc_shift(ct.shift, c, n - 4 * (w0 + kSegWords));
-        if (c) atomicXor(acc + f, c);
-    }
+    c = segment_to_end(ct, full, w0, n, c, seg_col, l);
+    if (l == 0 && c) atomicXor(acc + f, c);
 }
 
 // ---------------------------------------------------------------------------
@@ -148,6 +168,7 @@ __global__ void __launch_bounds__(32 * kEncWarps) k_encode_image_frames(ImageFra
     const uint64_t nw = ncrc / 4;          // full words; then the 2-byte tail at byte 4 nw
     const uint64_t w0 = ((uint64_t)blockIdx.x * kEncWarps + warp) * kSegWords;
     if (w0 > nw) return;
+    const uint32_t seg_col = seg_column(ct, w0, nw, l);
     uint8_t* out = a.frames + (size_t)f * a.frame_stride;
     uint32_t* ow = reinterpret_cast<uint32_t*>(out);
     const uint32_t* en = reinterpret_cast<const uint32_t*>(a.energies + (size_t)f * a.cells);
@@ -210,12 +231,8 @@ __global__ void __launch_bounds__(32 * kEncWarps) k_encode_image_frames(ImageFra
         const uint64_t end = cw0 + 32 <= nw ? 4 * (cw0 + 32) : ncrc;
         c = cw0 <= nw ? crc_shift(ct.shift, c, ncrc - end) : 0u;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
-    if (l == 0) {
-        if (full) c = crc_shift(ct.shift, c, ncrc - 4 * (w0 + kSegWords));
-        if (c) atomicXor(a.acc + f, c);
-    }
+    c = segment_to_end(ct, full, w0, ncrc, c, seg_col, l);
+    if (l == 0 && c) atomicXor(a.acc + f, c);
 }
 
 // crc[f] = acc[f] ^ k_n (k_n = A_n(~0) ^ ~0 from the host); optionally stored
@@ -331,6 +348,20 @@ uint32_t crc_advance_host(const uint32_t* shift, uint32_t v, uint64_t n) {
         }
     }
     return v;
+}
+
+std::vector<uint32_t> crc_segment_shifts_host(const uint32_t* shift, uint64_t n) {
+    const uint64_t segs = (n / 4) / kSegWords; // full segments: 4096 (s + 1) <= n
+    std::vector<uint32_t> t(segs * 32);
+    if (segs == 0) return t;
+    uint32_t col[32];
+    for (int b = 0; b < 32; ++b) col[b] = crc_advance_host(shift, 1u << b, n - 4 * kSegWords * segs);
+    for (uint64_t s = segs; s-- > 0;) {
+        for (int b = 0; b < 32; ++b) t[32 * s + b] = col[b];
+        if (s > 0)
+            for (int b = 0; b < 32; ++b) col[b] = crc_advance_host(shift, col[b], 4 * kSegWords);
+    }
+    return t;
 }
 
 uint32_t crc_init_term(const uint32_t* shift, uint64_t n) {

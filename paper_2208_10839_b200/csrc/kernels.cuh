@@ -18,6 +18,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace snb {
@@ -134,6 +135,8 @@ struct CrcTables {
     const uint32_t* slice;          // [4][256] slicing-by-4 tables
     const uint32_t* shift;          // [kCrcShiftMats][32] columns of A_{2^k}
     const uint32_t* lane;           // [32][32] columns of A_{128 (31 - l)} (warp-segment encoder)
+    const uint32_t* seg;            // [full segments][32] columns of A_{n - 4096 (s + 1)} for the
+                                    // launch's string length n (crc_segment_shifts_host), or null
 };
 struct FrameIds {                   // per-capture header fields
     uint32_t serial;
@@ -179,6 +182,10 @@ void crc_tables_host(uint32_t* slice, uint32_t* shift);
 uint32_t crc_init_term(const uint32_t* shift, uint64_t n);
 // A_n(v) on the host (shift: crc_tables_host's A_{2^k} columns)
 uint32_t crc_advance_host(const uint32_t* shift, uint32_t v, uint64_t n);
+// CrcTables::seg for strings of n bytes: per full 4 KB segment s the map that
+// moves its CRC to the string end (one warp-parallel step on the device
+// instead of a chain of up to log2(n) matrix products)
+std::vector<uint32_t> crc_segment_shifts_host(const uint32_t* shift, uint64_t n);
 
 // ---- tensor-core delay-and-sum (beamform_tc.cu) ---------------------------
 constexpr int kTcM = 128;      // directions per cluster (MMA M)

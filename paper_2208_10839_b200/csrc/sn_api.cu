@@ -209,6 +209,8 @@ struct sn_workspace {
     uint32_t* d_crc_slice = nullptr;
     uint32_t* d_crc_shift = nullptr;
     uint32_t* d_crc_lane = nullptr;
+    uint32_t* d_crc_seg_in = nullptr;  // CrcTables::seg for the input frames' CRC length
+    uint32_t* d_crc_seg_out = nullptr; // ... and the image frames'
     std::vector<uint32_t> h_crc_shift;
     uint8_t* d_img_tpl = nullptr;
     uint64_t img_tpl_len = 0, img_frame_len = 0, img_frame_stride = 0;
@@ -293,7 +295,7 @@ struct sn_workspace {
                         (void*)d_comp, (void*)d_comp32, (void*)d_shifts, (void*)d_ref_spec,
                         (void*)d_tw_mf, (void*)d_tw_env, (void*)d_tw_env32, (void*)d_tw_small, (void*)d_tw_small32, (void*)d_ff_u, (void*)d_ff_u32, (void*)d_ff_w, (void*)d_ff_w32, (void*)d_planes, (void*)d_dwords, (void*)d_resid,
                         (void*)d_tc_R, (void*)d_tc_base, (void*)d_amax, (void*)d_tc_start, (void*)d_tc_size,
-                        (void*)d_crc_slice, (void*)d_crc_shift, (void*)d_crc_lane, (void*)d_img_tpl, (void*)d_frames_out,
+                        (void*)d_crc_slice, (void*)d_crc_shift, (void*)d_crc_lane, (void*)d_crc_seg_in, (void*)d_crc_seg_out, (void*)d_img_tpl, (void*)d_frames_out,
                         (void*)d_frames_in, (void*)d_ids, (void*)d_crc_acc, (void*)d_crc_ok, (void*)d_bf_in, (void*)d_bf_out}) {
             if (p) cudaFree(p);
         }
@@ -581,6 +583,14 @@ struct sn_workspace {
         upload(d_img_tpl, tpl, stream);
         in_frame_len = 36 + 38 + packed_bytes + 4;
         in_frame_stride = (in_frame_len + 15) & ~uint64_t(15);
+        {
+            const auto si = crc_segment_shifts_host(h_crc_shift.data(), in_frame_len - 4);
+            const auto so = crc_segment_shifts_host(h_crc_shift.data(), img_frame_len - 4);
+            d_crc_seg_in = dmalloc<uint32_t>(std::max<size_t>(si.size(), 1), n);
+            d_crc_seg_out = dmalloc<uint32_t>(std::max<size_t>(so.size(), 1), n);
+            if (!si.empty()) upload(d_crc_seg_in, si, stream);
+            if (!so.empty()) upload(d_crc_seg_out, so, stream);
+        }
         const uint64_t B = max_batch;
         // output frames, host-side ids and CRC verdicts in two halves: the
         // blocks of one process_frames call alternate (block j + 1 is
@@ -595,7 +605,10 @@ struct sn_workspace {
         ck(cudaMallocHost(&h_ids, 2 * B * sizeof(FrameIds)), "cudaMallocHost");
         ck(cudaMallocHost(&h_crc_ok, 2 * B * sizeof(int32_t)), "cudaMallocHost");
     }
-    CrcTables crc_tables() const { return CrcTables{d_crc_slice, d_crc_shift, d_crc_lane}; }
+    // seg: the per-length segment maps of the input (false) or image (true) frames
+    CrcTables crc_tables(bool image) const {
+        return CrcTables{d_crc_slice, d_crc_shift, d_crc_lane, image ? d_crc_seg_out : d_crc_seg_in};
+    }
 
     // Tensor-core delay-and-sum setup (beamform_tc.cu): clusters of <= kTcM
     // consecutive slots cut greedily so that R_c (the largest per-channel
@@ -1187,9 +1200,9 @@ struct sn_workspace {
             ck(cudaStreamWaitEvent(stream, ev_in[0], 0), "wait");
             ck(cudaMemcpyAsync(d_ids, hid, c * sizeof(FrameIds), cudaMemcpyHostToDevice, stream), "H2D ids");
             ck(cudaMemsetAsync(d_crc_acc, 0, 2 * max_batch * sizeof(uint32_t), stream), "memset");
-            const CrcTables ct = crc_tables();
+            const CrcTables ct = crc_tables(true), ct_in = crc_tables(false);
             const uint64_t nin = in_frame_len - 4;
-            launch_crc_partial(d_frames_in, in_frame_stride, nin, c, ct, d_crc_acc, stream);
+            launch_crc_partial(d_frames_in, in_frame_stride, nin, c, ct_in, d_crc_acc, stream);
             launch_crc_finalize(d_crc_acc, crc_init_term(h_crc_shift.data(), nin), c, d_frames_in, in_frame_stride,
                                 nin, false, d_crc_ok, stream);
             ck(cudaMemcpyAsync(h_crc_ok + (uint64_t)half * max_batch, d_crc_ok, c * sizeof(int32_t),
