@@ -599,7 +599,7 @@ struct sn_workspace {
         d_frames_in = dmalloc<uint8_t>(B * in_frame_stride, n);
         d_ids = dmalloc<FrameIds>(B, n);
         d_crc_acc = dmalloc<uint32_t>(2 * B, n);
-        d_crc_ok = dmalloc<int32_t>(B, n);
+        d_crc_ok = dmalloc<int32_t>(2 * B, n);
         ck(cudaMallocHost(&h_frames_out, B * img_frame_len), "cudaMallocHost");
         ck(cudaMallocHost(&h_frames_in, B * in_frame_len), "cudaMallocHost");
         ck(cudaMallocHost(&h_ids, 2 * B * sizeof(FrameIds)), "cudaMallocHost");
@@ -1203,16 +1203,20 @@ struct sn_workspace {
             const CrcTables ct = crc_tables(true), ct_in = crc_tables(false);
             const uint64_t nin = in_frame_len - 4;
             launch_crc_partial(d_frames_in, in_frame_stride, nin, c, ct_in, d_crc_acc, stream);
+            int32_t* dok = d_crc_ok + (uint64_t)half * max_batch;
             launch_crc_finalize(d_crc_acc, crc_init_term(h_crc_shift.data(), nin), c, d_frames_in, in_frame_stride,
-                                nin, false, d_crc_ok, stream);
-            ck(cudaMemcpyAsync(h_crc_ok + (uint64_t)half * max_batch, d_crc_ok, c * sizeof(int32_t),
-                               cudaMemcpyDeviceToHost, stream), "D2H ok");
+                                nin, false, dok, stream);
             ck(cudaMemcpy2DAsync(d_packed, packed_bytes, d_frames_in + 74, in_frame_stride, packed_bytes, c,
                                  cudaMemcpyDeviceToDevice, stream), "D2D packed");
             enqueue_front(d_packed, 0, c, stream);
             ck(cudaEventRecord(ev_front, stream), "event");
-            ck(cudaEventRecord(ev_beams, stream), "event");
-            ck(cudaStreamWaitEvent(s_d2h, ev_beams, 0), "wait"); // the verdicts' download precedes ev_d2h
+            // the verdicts download on the D2H stream (a copy on the compute
+            // stream would queue behind the previous block's frame downloads
+            // on the copy engine and hold up this block's kernels); they
+            // precede ev_d2h[half], and dok is next written by block blk + 2
+            ck(cudaStreamWaitEvent(s_d2h, ev_front, 0), "wait");
+            ck(cudaMemcpyAsync(h_crc_ok + (uint64_t)half * max_batch, dok, c * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, s_d2h), "D2H ok");
             // envelope + frame encode in chunks; each chunk's frames download
             // (D2H stream) while the next chunk computes. D2H straight into the
             // caller's slots when they are page-locked and consecutive. The
