@@ -255,6 +255,26 @@ __global__ void k_crc_finalize(uint32_t* acc, uint32_t k_n, uint64_t count, uint
     }
 }
 
+// The packed bits of `count` received frames (at src + f * sstride, 2-byte
+// aligned: byte 74 of a 16-byte aligned frame) into the 4-byte aligned capture
+// buffer (dst + f * nbytes, nbytes % 4 == 0): one output word per thread from
+// two 16-bit loads. A kernel rather than a 2-D device-to-device memcpy, which
+// can queue on a copy engine behind the previous block's downloads.
+__global__ void k_unpack_frames(const uint8_t* __restrict__ src, uint64_t sstride, uint8_t* __restrict__ dst,
+                                uint64_t nbytes) {
+    const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; // output word
+    if (4 * j >= nbytes) return;
+    const uint16_t* s = reinterpret_cast<const uint16_t*>(src + (size_t)blockIdx.y * sstride) + 2 * j;
+    reinterpret_cast<uint32_t*>(dst + (size_t)blockIdx.y * nbytes)[j] = (uint32_t)__ldg(s) | ((uint32_t)__ldg(s + 1) << 16);
+}
+
+void launch_unpack_frames(const uint8_t* src, uint64_t sstride, uint8_t* dst, uint64_t nbytes, uint64_t count,
+                          cudaStream_t s) {
+    if (count == 0 || nbytes == 0) return;
+    k_unpack_frames<<<dim3((unsigned)((nbytes / 4 + 255) / 256), (unsigned)count), 256, 0, s>>>(src, sstride, dst,
+                                                                                                 nbytes);
+}
+
 void launch_crc_partial(const uint8_t* base, uint64_t stride, uint64_t n, uint64_t count, const CrcTables& ct,
                         uint32_t* acc, cudaStream_t s) {
     if (n == 0 || count == 0) return;

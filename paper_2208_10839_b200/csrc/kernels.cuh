@@ -153,6 +153,8 @@ struct ImageFrameArgs {
 void launch_crc_partial(const uint8_t* base, uint64_t stride, uint64_t n, uint64_t count, const CrcTables& ct,
                         uint32_t* acc, cudaStream_t s);
 void launch_encode_image_frames(const ImageFrameArgs& a, uint64_t count, const CrcTables& ct, cudaStream_t s);
+void launch_unpack_frames(const uint8_t* src, uint64_t sstride, uint8_t* dst, uint64_t nbytes, uint64_t count,
+                          cudaStream_t s);
 void launch_crc_finalize(uint32_t* acc, uint32_t k_n, uint64_t count, uint8_t* out, uint64_t stride, uint64_t n,
                          bool store, int32_t* ok, cudaStream_t s);
 uint32_t crc32_host(const uint8_t* p, uint64_t n);

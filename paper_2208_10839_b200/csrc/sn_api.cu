@@ -597,7 +597,7 @@ struct sn_workspace {
         // enqueued while block j's frames download)
         d_frames_out = dmalloc<uint8_t>(2 * B * img_frame_stride, n);
         d_frames_in = dmalloc<uint8_t>(B * in_frame_stride, n);
-        d_ids = dmalloc<FrameIds>(B, n);
+        d_ids = dmalloc<FrameIds>(2 * B, n);
         d_crc_acc = dmalloc<uint32_t>(2 * B, n);
         d_crc_ok = dmalloc<int32_t>(2 * B, n);
         ck(cudaMallocHost(&h_frames_out, B * img_frame_len), "cudaMallocHost");
@@ -1196,9 +1196,12 @@ struct sn_workspace {
                 std::memcpy(&id.seq, f + 48, 8);
                 hid[i] = id;
             }
+            // ids on the copy stream too (an upload on the compute stream can
+            // queue behind the next upload); d_ids alternates halves
+            FrameIds* did = d_ids + (uint64_t)half * max_batch;
+            ck(cudaMemcpyAsync(did, hid, c * sizeof(FrameIds), cudaMemcpyHostToDevice, s_h2d), "H2D ids");
             ck(cudaEventRecord(ev_in[0], s_h2d), "event");
             ck(cudaStreamWaitEvent(stream, ev_in[0], 0), "wait");
-            ck(cudaMemcpyAsync(d_ids, hid, c * sizeof(FrameIds), cudaMemcpyHostToDevice, stream), "H2D ids");
             ck(cudaMemsetAsync(d_crc_acc, 0, 2 * max_batch * sizeof(uint32_t), stream), "memset");
             const CrcTables ct = crc_tables(true), ct_in = crc_tables(false);
             const uint64_t nin = in_frame_len - 4;
@@ -1206,8 +1209,7 @@ struct sn_workspace {
             int32_t* dok = d_crc_ok + (uint64_t)half * max_batch;
             launch_crc_finalize(d_crc_acc, crc_init_term(h_crc_shift.data(), nin), c, d_frames_in, in_frame_stride,
                                 nin, false, dok, stream);
-            ck(cudaMemcpy2DAsync(d_packed, packed_bytes, d_frames_in + 74, in_frame_stride, packed_bytes, c,
-                                 cudaMemcpyDeviceToDevice, stream), "D2D packed");
+            launch_unpack_frames(d_frames_in + 74, in_frame_stride, d_packed, packed_bytes, c, stream);
             enqueue_front(d_packed, 0, c, stream);
             ck(cudaEventRecord(ev_front, stream), "event");
             // the verdicts download on the D2H stream (a copy on the compute
@@ -1224,7 +1226,7 @@ struct sn_workspace {
             const uint64_t nout = img_frame_len - 4;
             const uint32_t kout = crc_init_term(h_crc_shift.data(), nout);
             enqueue_per_direction(c, [&](uint64_t off, uint64_t k, cudaStream_t cs, cudaEvent_t ed) {
-                ImageFrameArgs ia{d_energy + off * energy_per, d_img_tpl, d_ids + off,
+                ImageFrameArgs ia{d_energy + off * energy_per, d_img_tpl, did + off,
                                   dfo + off * img_frame_stride, d_crc_acc + max_batch + off, energy_per,
                                   img_tpl_len, img_frame_len, img_frame_stride};
                 launch_encode_image_frames(ia, k, ct, cs);
