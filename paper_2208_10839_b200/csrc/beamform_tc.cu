@@ -158,8 +158,12 @@ template <int TN> constexpr int slots_for() { return TN == 64 ? 8 : TN == 96 ? 5
 // B window buffers (loads run kWin - 1 tiles ahead); 2 for N = 128, whose
 // epilogue parks Y_hi in shared memory
 constexpr int win_for(int tn) { return tn == 128 ? 2 : 3; }
-constexpr int kEpiWarps = 16;                  // epilogue warps; warp 8 produces and issues
-constexpr int kTcThreads = 32 * (kEpiWarps + 1);
+constexpr int kEpiWarps = 16;                  // epilogue warps; warp kEpiWarps produces and issues
+#ifndef SNB_TC_EPI_W96
+#define SNB_TC_EPI_W96 12 // N = 96: 12 epilogue warps (13 warps: 128 registers; 16: 96, beamform stage +1%)
+#endif
+template <int TN> constexpr int epi_warps() { return TN == 96 ? SNB_TC_EPI_W96 : kEpiWarps; }
+template <int TN> constexpr int tc_threads() { return 32 * (epi_warps<TN>() + 1); }
 constexpr int kTmemCols = 512;
 constexpr int kABytes = 2 * kTcM * 16; // one shift: two channel halves x 128 rows x 16 B
 
@@ -273,7 +277,8 @@ __device__ unsigned long long g_tc_times[4 * 1024];
 #endif
 
 template <int TN>
-__global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const __grid_constant__ TcSched sched) {
+__global__ void __launch_bounds__(tc_threads<TN>(), 1) k_beamform_tc(TcArgs a, const __grid_constant__ TcSched sched) {
+    constexpr int EW = epi_warps<TN>();
 #ifdef SNB_TC_EXP_TIMES
     unsigned long long t_start;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
@@ -302,7 +307,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
     }
     if (tid == 0) {
         for (int i = 0; i < kWin; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wfree[i], 1); }
-        for (int i = 0; i < kSlots; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], kEpiWarps); }
+        for (int i = 0; i < kSlots; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], EW); }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -318,7 +323,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
 #endif
     const int ntile = t_end - t_beg;
 
-    if (warp == kEpiWarps) {
+    if (warp == EW) {
         // ===================== producer / MMA issuer warp =====================
         const uint32_t idesc = idesc_i8(kTcM, TN);
         const uint32_t ares_addr = su32(Ares), bw_addr = su32(Bw);
@@ -431,7 +436,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
         // warp w: TMEM lane quarter w & 3 (directions), column quarter w >> 2
         const int quarter = warp & 3, colq = warp >> 2;
         const int d = quarter * 32 + lane;
-        constexpr int NC = TN / 4; // columns per thread
+        constexpr int NC = TN / (EW / 4); // columns per thread
         constexpr bool kPark = TN == 128; // Y_hi parked in shared memory (register budget)
         static_assert(NC % 8 == 0 && (!kPark || NC == 32), "epilogue column chunks");
         const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
@@ -562,7 +567,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_beamform_tc(TcArgs a, const _
         }
     }
 #ifdef SNB_TC_EXP_TIMES
-    if (warp == kEpiWarps) {
+    if (warp == EW) {
         unsigned long long t_fin;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_fin));
         unsigned sr = 0, sw = 0;
@@ -615,9 +620,9 @@ cudaError_t launch_beamform_tc(const TcArgs& a, const TcSched& sched, int grid, 
                    : a.n == 96  ? (const void*)k_beamform_tc<96>
                                 : (const void*)k_beamform_tc<64>;
     set_smem(fn, smem);
-    if (a.n == 128) k_beamform_tc<128><<<grid, kTcThreads, smem, s>>>(a, sched);
-    else if (a.n == 96) k_beamform_tc<96><<<grid, kTcThreads, smem, s>>>(a, sched);
-    else k_beamform_tc<64><<<grid, kTcThreads, smem, s>>>(a, sched);
+    if (a.n == 128) k_beamform_tc<128><<<grid, tc_threads<128>(), smem, s>>>(a, sched);
+    else if (a.n == 96) k_beamform_tc<96><<<grid, tc_threads<96>(), smem, s>>>(a, sched);
+    else k_beamform_tc<64><<<grid, tc_threads<64>(), smem, s>>>(a, sched);
     return cudaPeekAtLastError();
 }
 
