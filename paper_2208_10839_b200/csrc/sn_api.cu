@@ -148,17 +148,22 @@ struct sn_workspace {
     static constexpr int kMaxChunks = 16;
     // envelope chunk sizes of a block of c captures: ~2 per chunk, the last
     // chunk a single capture (its download is the exposed one)
-    static std::vector<uint64_t> env_chunks(uint64_t c) {
+#ifndef SNB_ENV_SUB
+#define SNB_ENV_SUB 2 // captures per envelope sub-chunk (the last one: 1)
+#endif
+#ifndef SNB_ENV_SUB_FRAMES
+// the frame path: 3 per chunk (an encoder launch per chunk between the
+// envelope chunks; e2e_wire A/B 2 / 3 / 4: 3,502 / 3,557-3,564 / 3,513-3,518 /s)
+#define SNB_ENV_SUB_FRAMES 3
+#endif
+    static std::vector<uint64_t> env_chunks(uint64_t c, uint64_t sub = SNB_ENV_SUB) {
         std::vector<uint64_t> v;
         if (c <= 2) {
             v.assign(c, 1);
             return v;
         }
-#ifndef SNB_ENV_SUB
-#define SNB_ENV_SUB 2 // captures per envelope sub-chunk (the last one: 1)
-#endif
         uint64_t rest = c - 1;
-        const uint64_t n = std::min<uint64_t>((rest + SNB_ENV_SUB - 1) / SNB_ENV_SUB, kMaxChunks - 1);
+        const uint64_t n = std::min<uint64_t>((rest + sub - 1) / sub, kMaxChunks - 1);
         for (uint64_t j = 0; j < n; ++j) v.push_back(rest / n + (j < rest % n ? 1 : 0));
         v.push_back(1);
         return v;
@@ -986,7 +991,8 @@ struct sn_workspace {
     // sub-chunk's stream and returns its launch count. A later chunk's
     // delay-and-sum waits until the ring's previous contents are read.
     template <typename After>
-    uint64_t enqueue_per_direction(uint64_t c, After&& after, cudaEvent_t energies_free = nullptr) {
+    uint64_t enqueue_per_direction(uint64_t c, After&& after, cudaEvent_t energies_free = nullptr,
+                                   uint64_t sub = SNB_ENV_SUB) {
         uint64_t nlaunch = 0, ev_j = 0;
         for (uint64_t o = 0; o < c; o += chunk_cap) {
             const uint64_t kc = std::min(chunk_cap, c - o);
@@ -1000,7 +1006,7 @@ struct sn_workspace {
             // sub-chunks on two streams (measured: also for the inner blocks of
             // a pipelined call, where one launch per block was 2% slower: the
             // next block's front end starts under the other stream's tail)
-            const std::vector<uint64_t> chunks = env_chunks(kc);
+            const std::vector<uint64_t> chunks = env_chunks(kc, sub);
             uint64_t off = 0;
             for (uint64_t j = 0; j < chunks.size(); ++j, ++ev_j) {
                 const uint64_t k = chunks[j];
@@ -1241,7 +1247,7 @@ struct sn_workspace {
                                        cudaMemcpyDeviceToHost, s_d2h), "D2H frame");
                 }
                 return uint64_t{2};
-            }, blk >= 2 ? ev_d2h[half] : nullptr);
+            }, blk >= 2 ? ev_d2h[half] : nullptr, SNB_ENV_SUB_FRAMES);
             ck(cudaEventRecord(ev_d2h[half], s_d2h), "event");
             ck(cudaGetLastError(), "frame kernels");
             pend[half] = batch;
